@@ -1,0 +1,1252 @@
+// capi.cu -- the C ABI (include/ffsga_cuda.h): handles, device memory, launch sequences.
+//
+// Host code here only validates, lays data out for the device and sequences launches; every
+// evaluation, breeding step, replacement, archive update and migration runs in kernels.cu.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ffsga_cuda.h"
+#include "launch.h"
+
+using namespace ffsga_dev;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, std::string msg) { throw Fail{code, std::move(msg)}; }
+
+#define CK(x)                                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess) fail(FFSGA_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return FFSGA_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FFSGA_ERR_CUDA;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t n) {
+        release();
+        if (n == 0) n = 16;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            fail(e == cudaErrorMemoryAllocation ? FFSGA_ERR_OOM : FFSGA_ERR_CUDA,
+                 std::string("device allocation of ") + std::to_string(n) + " bytes failed: " + cudaGetErrorString(e));
+        }
+        bytes = n;
+    }
+    void ensure(size_t n) {
+        if (n > bytes) alloc(n);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+template <typename T>
+void upload(DevBuf& b, const std::vector<T>& v) {
+    b.alloc(sizeof(T) * std::max<size_t>(v.size(), 1));
+    if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+}
+
+unsigned long long coin_threshold(double p) {  // (u>>11) < ceil(p * 2^53)  <=>  unit(u) < p
+    return (unsigned long long)std::ceil(p * 9007199254740992.0);
+}
+
+int bit_width_u(unsigned v) {
+    int w = 0;
+    while (v) {
+        ++w;
+        v >>= 1;
+    }
+    return w;
+}
+
+std::string gene_error(unsigned long long code) {
+    const int stage = (int)((code >> 16) & 0xFFFFull);
+    const int job = (int)(code & 0xFFFFull);
+    return "decode: machine index out of range at job " + std::to_string(job) + " stage " + std::to_string(stage);
+}
+
+constexpr unsigned long long kNoError = ~0ull;
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ instance
+struct ffsga_cuda_instance_t {
+    int device = 0;
+    int sm_count = 0;
+    int J = 0, S = 0, Jpad = 0, maxM = 0;
+    std::vector<int> M, stage_off, bps, sbo;
+    int bpj = 0, total_bits = 0, words = 0;
+    double weight = 0, emax = 0;
+    DevInst d{};
+    DevBuf dM, dStageOff, dBps, dSbo, dProcT, dRelease, dDue, dRelOrder, dBitStage;
+    EvalConfig ec{};
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    // joint-step work list
+    DevBuf wl_ptrs, wl_obj, wl_fit, wl_count, wl_scratch, cell_desc, pseudo_desc;
+    // evaluate() staging
+    DevBuf ev_in, ev_rows, ev_obj, ev_fit, ev_mk, ev_td, ev_err;
+    long long ev_cap = 0;
+    // migration scratch
+    DevBuf mg_keys0, mg_keys1, mg_idx0, mg_idx_a, mg_idx_b, mg_temp;
+    // timing
+    bool timing = false;
+    double t_ms[3] = {0, 0, 0};
+    long long t_n[3] = {0, 0, 0};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    size_t block() const { return (size_t)S * Jpad; }
+    void use() const { CK(cudaSetDevice(device)); }
+    ~ffsga_cuda_instance_t() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamDestroy(stream);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+    // brackets a launch with events when timing is enabled
+    template <typename F>
+    void timed(int which, F&& f) {
+        if (!timing) {
+            f();
+            return;
+        }
+        CK(cudaEventRecord(ev0, stream));
+        f();
+        CK(cudaEventRecord(ev1, stream));
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        t_ms[which] += ms;
+        t_n[which] += 1;
+    }
+};
+
+namespace {
+
+// Evaluate n device rows into device outputs; returns the first gene error code or kNoError.
+void eval_rows(ffsga_cuda_instance_t* I, const uint8_t* rows, long long n, double* obj, double* fit, double* mk,
+               double* td, bool check) {
+    if (n <= 0) return;
+    I->ev_err.ensure(sizeof(unsigned long long));
+    if (check) CK(cudaMemsetAsync(I->ev_err.p, 0xFF, sizeof(unsigned long long), I->stream));
+    EvalItems W{};
+    W.n = n;
+    W.base = rows;
+    W.stride = (long long)I->block();
+    W.obj = obj;
+    W.fit = fit;
+    W.mk = mk;
+    W.td = td;
+    W.err = I->ev_err.as<unsigned long long>();
+    I->timed(0, [&] { CK(launch_eval(I->d, I->ec, W, n, I->sm_count, false, I->stream)); });
+    g_launches += 1;
+}
+
+unsigned long long read_error(ffsga_cuda_instance_t* I) {
+    unsigned long long code = kNoError;
+    CK(cudaMemcpyAsync(&code, I->ev_err.p, sizeof(code), cudaMemcpyDeviceToHost, I->stream));
+    CK(cudaStreamSynchronize(I->stream));
+    return code;
+}
+
+void ensure_eval_staging(ffsga_cuda_instance_t* I, long long chunk) {
+    if (chunk <= I->ev_cap) return;
+    const size_t L = (size_t)I->J * I->S;
+    I->ev_in.alloc(chunk * L * sizeof(int32_t));
+    I->ev_rows.alloc(chunk * I->block());
+    I->ev_obj.alloc(chunk * sizeof(double));
+    I->ev_fit.alloc(chunk * sizeof(double));
+    I->ev_mk.alloc(chunk * sizeof(double));
+    I->ev_td.alloc(chunk * sizeof(double));
+    I->ev_cap = chunk;
+}
+
+template <typename T>
+void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* obj, double* fit, double* mk,
+                   double* td) {
+    if (n < 0) fail(FFSGA_ERR_CONTRACT, "evaluate: negative batch size");
+    if (n == 0) return;
+    if (!genes || !obj || !fit) fail(FFSGA_ERR_ARG, "evaluate: null pointer");
+    const long long L = (long long)I->J * I->S;
+    const long long chunk = std::min<long long>(n, 1 << 16);
+    ensure_eval_staging(I, chunk);
+    for (long long first = 0; first < n; first += chunk) {
+        const long long c = std::min<long long>(chunk, n - first);
+        CK(cudaMemcpyAsync(I->ev_in.p, genes + first * L, sizeof(T) * c * L, cudaMemcpyHostToDevice, I->stream));
+        if (sizeof(T) == 4)
+            CK(launch_rows_from_int(I->d, I->ev_in.as<int32_t>(), nullptr, I->ev_rows.as<uint8_t>(), c, I->stream));
+        else
+            CK(launch_rows_from_int(I->d, nullptr, I->ev_in.as<uint8_t>(), I->ev_rows.as<uint8_t>(), c, I->stream));
+        g_launches += 1;
+        eval_rows(I, I->ev_rows.as<uint8_t>(), c, I->ev_obj.as<double>(), I->ev_fit.as<double>(),
+                  I->ev_mk.as<double>(), I->ev_td.as<double>(), true);
+        CK(cudaMemcpyAsync(obj + first, I->ev_obj.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(fit + first, I->ev_fit.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
+        if (mk) CK(cudaMemcpyAsync(mk + first, I->ev_mk.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
+        if (td) CK(cudaMemcpyAsync(td + first, I->ev_td.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
+        const unsigned long long code = read_error(I);
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ffsga_cuda_last_error(void) { return g_err.c_str(); }
+int ffsga_cuda_abi_version(void) { return FFSGA_CUDA_ABI_VERSION; }
+
+int ffsga_cuda_device_count(int* count) {
+    return guard([&] {
+        if (!count) fail(FFSGA_ERR_ARG, "null pointer");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *count = n;
+    });
+}
+
+int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const int32_t* machines,
+                               const double* proc, const double* release, const double* due, double weight,
+                               double emax, ffsga_cuda_instance* out) {
+    return guard([&] {
+        if (!out || !machines || !proc || !release || !due) fail(FFSGA_ERR_ARG, "instance_create: null pointer");
+        *out = nullptr;
+        if (num_jobs < 1) fail(FFSGA_ERR_CONTRACT, "instance: num_jobs must be >= 1");
+        if (num_stages < 1) fail(FFSGA_ERR_CONTRACT, "instance: num_stages must be >= 1");
+        if (num_jobs > 64000) fail(FFSGA_ERR_CONFIG, "device decoder supports at most 64000 jobs");
+        if (num_stages > 65535) fail(FFSGA_ERR_CONFIG, "device decoder supports at most 65535 stages");
+        int dev_count = 0;
+        cudaError_t e = cudaGetDeviceCount(&dev_count);
+        if (e != cudaSuccess || dev_count == 0) {
+            cudaGetLastError();
+            fail(FFSGA_ERR_CUDA, "no CUDA device available: the FFS hot path runs only on sm_100 GPUs");
+        }
+        if (device < 0 || device >= dev_count) fail(FFSGA_ERR_ARG, "instance_create: bad device ordinal");
+        auto* I = new ffsga_cuda_instance_t();
+        std::unique_ptr<ffsga_cuda_instance_t> hold(I);
+        I->device = device;
+        I->use();
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) fail(FFSGA_ERR_CUDA, "device is not sm_100 class (built for sm_100a only)");
+        I->sm_count = prop.multiProcessorCount;
+        const int J = num_jobs, S = num_stages;
+        I->J = J;
+        I->S = S;
+        I->Jpad = (J + 15) & ~15;
+        I->M.assign(machines, machines + S);
+        I->stage_off.assign(S + 1, 0);
+        I->maxM = 0;
+        for (int s = 0; s < S; ++s) {
+            if (I->M[s] < 1) fail(FFSGA_ERR_CONTRACT, "instance: every stage needs at least one machine");
+            if (I->M[s] > kMaxMachines)
+                fail(FFSGA_ERR_CONFIG, "device decoder supports at most 32 machines per stage");
+            I->stage_off[s + 1] = I->stage_off[s] + I->M[s];
+            I->maxM = std::max(I->maxM, I->M[s]);
+        }
+        const int MT = I->stage_off[S];
+        double horizon = 0.0, min_p = INFINITY;
+        for (int j = 0; j < J; ++j) horizon = std::max(horizon, release[j]);
+        for (int j = 0; j < J; ++j)
+            for (int s = 0; s < S; ++s) {
+                double worst = 0.0;
+                for (int m = 0; m < I->M[s]; ++m) {
+                    const double p = proc[(size_t)j * MT + I->stage_off[s] + m];
+                    if (!(p > 0.0) || !std::isfinite(p))
+                        fail(FFSGA_ERR_CONTRACT, "instance: processing times must be positive");
+                    worst = std::max(worst, p);
+                    min_p = std::min(min_p, p);
+                }
+                horizon += worst;
+            }
+        for (int j = 0; j < J; ++j)
+            if (!std::isfinite(release[j]) || !std::isfinite(due[j]))
+                fail(FFSGA_ERR_CONTRACT, "instance: release and due times must be finite");
+        // completions on a machine must strictly increase for the merge-ordered decoder:
+        // x + p > x for every completion x <= horizon iff p >= ulp(horizon)
+        const double ulp = std::nextafter(horizon, INFINITY) - horizon;
+        if (!(min_p >= ulp))
+            fail(FFSGA_ERR_CONFIG, "device decoder needs processing times >= ulp(schedule horizon)");
+        I->weight = weight;
+        I->emax = emax;
+        // stage-major proc columns with one zero pad per column
+        std::vector<double> procT((size_t)MT * (J + 1), 0.0);
+        for (int j = 0; j < J; ++j)
+            for (int s = 0; s < S; ++s)
+                for (int m = 0; m < I->M[s]; ++m)
+                    procT[(size_t)(I->stage_off[s] + m) * (J + 1) + j] = proc[(size_t)j * MT + I->stage_off[s] + m];
+        // stage-0 order: jobs by (release, index)  (model.cpp:98-105)
+        std::vector<uint16_t> order(J);
+        std::iota(order.begin(), order.end(), 0);
+        std::sort(order.begin(), order.end(), [&](int a, int b) {
+            return release[a] < release[b] || (release[a] == release[b] && a < b);
+        });
+        // bit layout (chromosome.cpp:10-26)
+        I->bps.assign(S, 0);
+        I->sbo.assign(S + 1, 0);
+        for (int s = 0; s < S; ++s) {
+            I->bps[s] = std::max(1, bit_width_u((unsigned)I->M[s] - 1u));
+            I->sbo[s + 1] = I->sbo[s] + I->bps[s];
+        }
+        I->bpj = I->sbo[S];
+        const long long tb = (long long)J * I->bpj;
+        if (tb > 0x7FFFFFFF) fail(FFSGA_ERR_CONFIG, "bit layout too large");
+        I->total_bits = (int)tb;
+        I->words = std::max(1, (I->total_bits + 63) / 64);
+        std::vector<uint16_t> bit_stage(I->bpj);
+        for (int s = 0; s < S; ++s)
+            for (int r = I->sbo[s]; r < I->sbo[s + 1]; ++r) bit_stage[r] = (uint16_t)s;
+        upload(I->dM, I->M);
+        upload(I->dStageOff, I->stage_off);
+        upload(I->dBps, I->bps);
+        upload(I->dSbo, I->sbo);
+        upload(I->dProcT, procT);
+        upload(I->dRelease, std::vector<double>(release, release + J));
+        upload(I->dDue, std::vector<double>(due, due + J));
+        upload(I->dRelOrder, order);
+        upload(I->dBitStage, bit_stage);
+        DevInst& d = I->d;
+        d.J = J;
+        d.S = S;
+        d.Jpad = I->Jpad;
+        d.maxM = I->maxM;
+        d.bits_per_job = I->bpj;
+        d.total_bits = I->total_bits;
+        d.words = I->words;
+        d.weight = weight;
+        d.emax = emax;
+        d.M = I->dM.as<int>();
+        d.stage_off = I->dStageOff.as<int>();
+        d.bps = I->dBps.as<int>();
+        d.sbo = I->dSbo.as<int>();
+        d.procT = I->dProcT.as<double>();
+        d.release = I->dRelease.as<double>();
+        d.due = I->dDue.as<double>();
+        d.rel_order = I->dRelOrder.as<uint16_t>();
+        const int rc = eval_config(d, I->sm_count, &I->ec);
+        if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
+        if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
+        CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&I->ev0));
+        CK(cudaEventCreate(&I->ev1));
+        I->wl_count.alloc(sizeof(long long));
+        *out = hold.release();
+    });
+}
+
+int ffsga_cuda_instance_destroy(ffsga_cuda_instance inst) {
+    return guard([&] { delete inst; });
+}
+
+int ffsga_cuda_instance_info(ffsga_cuda_instance inst, int* row_stride, int* group_lanes, int* total_bits,
+                             int* smem_per_group) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        if (row_stride) *row_stride = inst->Jpad;
+        if (group_lanes) *group_lanes = inst->ec.G;
+        if (total_bits) *total_bits = inst->total_bits;
+        if (smem_per_group) *smem_per_group = inst->ec.gl.bytes;
+    });
+}
+
+int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t n, double* obj, double* fit,
+                        double* mk, double* td) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        evaluate_host(inst, genes, n, obj, fit, mk, td);
+    });
+}
+
+int ffsga_cuda_evaluate_u8(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* obj, double* fit,
+                           double* mk, double* td) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        evaluate_host(inst, genes, n, obj, fit, mk, td);
+    });
+}
+
+int ffsga_cuda_decode(ffsga_cuda_instance inst, const int32_t* genes, int32_t* machine, double* start,
+                      double* completion, double* report5) {
+    return guard([&] {
+        if (!inst || !genes || !machine || !start || !completion) fail(FFSGA_ERR_ARG, "decode: null pointer");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        ffsga_cuda_instance_t* I = inst;
+        const size_t L = (size_t)I->J * I->S;
+        ensure_eval_staging(I, 1);
+        DevBuf sm, ss, sc;
+        sm.alloc(L * sizeof(int32_t));
+        ss.alloc(L * sizeof(double));
+        sc.alloc(L * sizeof(double));
+        CK(cudaMemcpyAsync(I->ev_in.p, genes, L * sizeof(int32_t), cudaMemcpyHostToDevice, I->stream));
+        CK(launch_rows_from_int(I->d, I->ev_in.as<int32_t>(), nullptr, I->ev_rows.as<uint8_t>(), 1, I->stream));
+        I->ev_err.ensure(sizeof(unsigned long long));
+        CK(cudaMemsetAsync(I->ev_err.p, 0xFF, sizeof(unsigned long long), I->stream));
+        EvalItems W{};
+        W.n = 1;
+        W.base = I->ev_rows.as<uint8_t>();
+        W.stride = (long long)I->block();
+        W.obj = I->ev_obj.as<double>();
+        W.fit = I->ev_fit.as<double>();
+        W.mk = I->ev_mk.as<double>();
+        W.td = I->ev_td.as<double>();
+        W.err = I->ev_err.as<unsigned long long>();
+        W.smachine = sm.as<int>();
+        W.sstart = ss.as<double>();
+        W.scomp = sc.as<double>();
+        CK(launch_eval(I->d, I->ec, W, 1, I->sm_count, true, I->stream));
+        g_launches += 2;
+        const unsigned long long code = read_error(I);
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        CK(cudaMemcpy(machine, sm.p, L * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(start, ss.p, L * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(completion, sc.p, L * sizeof(double), cudaMemcpyDeviceToHost));
+        if (report5) {
+            double r[4];
+            CK(cudaMemcpy(&r[0], I->ev_mk.p, sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&r[1], I->ev_td.p, sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&r[2], I->ev_obj.p, sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&r[3], I->ev_fit.p, sizeof(double), cudaMemcpyDeviceToHost));
+            report5[0] = r[0];
+            report5[1] = r[1];
+            report5[2] = r[2];
+            report5[3] = r[3];
+            report5[4] = I->emax;
+        }
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ batches
+struct ffsga_cuda_batch_t {
+    ffsga_cuda_instance_t* inst = nullptr;
+    long long cap = 0;
+    DevBuf rows, obj, fit, mk, td, err, stage;
+    long long stage_cap = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~ffsga_cuda_batch_t() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+namespace {
+template <typename T>
+void batch_upload(ffsga_cuda_batch b, const T* genes, int64_t n) {
+    if (!b || !genes) fail(FFSGA_ERR_ARG, "batch_upload: null pointer");
+    if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_upload: n exceeds capacity");
+    auto* I = b->inst;
+    I->use();
+    const long long L = (long long)I->J * I->S;
+    const long long chunk = std::min<long long>(std::max<long long>(n, 1), 1 << 14);
+    if (chunk * L * (long long)sizeof(T) > (long long)b->stage.bytes) b->stage.alloc(chunk * L * sizeof(T));
+    for (long long f = 0; f < n; f += chunk) {
+        const long long c = std::min<long long>(chunk, n - f);
+        CK(cudaMemcpyAsync(b->stage.p, genes + f * L, sizeof(T) * c * L, cudaMemcpyHostToDevice, I->stream));
+        uint8_t* dst = b->rows.as<uint8_t>() + (size_t)f * I->block();
+        if (sizeof(T) == 4)
+            CK(launch_rows_from_int(I->d, b->stage.as<int32_t>(), nullptr, dst, c, I->stream));
+        else
+            CK(launch_rows_from_int(I->d, nullptr, b->stage.as<uint8_t>(), dst, c, I->stream));
+        g_launches += 1;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffsga_cuda_batch_create(ffsga_cuda_instance inst, int64_t capacity, ffsga_cuda_batch* out) {
+    return guard([&] {
+        if (!inst || !out) fail(FFSGA_ERR_ARG, "batch_create: null pointer");
+        if (capacity < 1) fail(FFSGA_ERR_CONTRACT, "batch capacity must be >= 1");
+        inst->use();
+        auto* b = new ffsga_cuda_batch_t();
+        std::unique_ptr<ffsga_cuda_batch_t> hold(b);
+        b->inst = inst;
+        b->cap = capacity;
+        b->rows.alloc((size_t)capacity * inst->block());
+        b->obj.alloc(sizeof(double) * capacity);
+        b->fit.alloc(sizeof(double) * capacity);
+        b->mk.alloc(sizeof(double) * capacity);
+        b->td.alloc(sizeof(double) * capacity);
+        b->err.alloc(sizeof(unsigned long long));
+        CK(cudaMemset(b->err.p, 0xFF, sizeof(unsigned long long)));
+        CK(cudaEventCreate(&b->e0));
+        CK(cudaEventCreate(&b->e1));
+        *out = hold.release();
+    });
+}
+
+int ffsga_cuda_batch_destroy(ffsga_cuda_batch b) {
+    return guard([&] { delete b; });
+}
+
+int ffsga_cuda_batch_fill_random(ffsga_cuda_batch b, uint64_t base_seed, int64_t first, int64_t n) {
+    return guard([&] {
+        if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_fill_random: n exceeds capacity");
+        auto* I = b->inst;
+        I->use();
+        CK(launch_random_rows(I->d, b->rows.as<uint8_t>(), (long long)I->block(), n, base_seed, first, true, I->stream));
+        g_launches += 1;
+    });
+}
+
+int ffsga_cuda_batch_upload(ffsga_cuda_batch b, const int32_t* genes, int64_t n) {
+    return guard([&] { batch_upload(b, genes, n); });
+}
+
+int ffsga_cuda_batch_upload_u8(ffsga_cuda_batch b, const uint8_t* genes, int64_t n) {
+    return guard([&] { batch_upload(b, genes, n); });
+}
+
+int ffsga_cuda_batch_evaluate(ffsga_cuda_batch b, int64_t n) {
+    return guard([&] {
+        if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_evaluate: n exceeds capacity");
+        auto* I = b->inst;
+        I->use();
+        EvalItems W{};
+        W.n = n;
+        W.base = b->rows.as<uint8_t>();
+        W.stride = (long long)I->block();
+        W.obj = b->obj.as<double>();
+        W.fit = b->fit.as<double>();
+        W.mk = b->mk.as<double>();
+        W.td = b->td.as<double>();
+        W.err = b->err.as<unsigned long long>();
+        CK(cudaEventRecord(b->e0, I->stream));
+        CK(launch_eval(I->d, I->ec, W, n, I->sm_count, false, I->stream));
+        CK(cudaEventRecord(b->e1, I->stream));
+        g_launches += 1;
+    });
+}
+
+int ffsga_cuda_batch_last_eval_ms(ffsga_cuda_batch b, float* ms) {
+    return guard([&] {
+        if (!b || !ms) fail(FFSGA_ERR_ARG, "null pointer");
+        b->inst->use();
+        CK(cudaEventSynchronize(b->e1));
+        CK(cudaEventElapsedTime(ms, b->e0, b->e1));
+    });
+}
+
+int ffsga_cuda_batch_results(ffsga_cuda_batch b, int64_t n, double* obj, double* fit, double* mk, double* td) {
+    return guard([&] {
+        if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_results: n exceeds capacity");
+        auto* I = b->inst;
+        I->use();
+        const size_t bytes = sizeof(double) * n;
+        if (obj) CK(cudaMemcpyAsync(obj, b->obj.p, bytes, cudaMemcpyDeviceToHost, I->stream));
+        if (fit) CK(cudaMemcpyAsync(fit, b->fit.p, bytes, cudaMemcpyDeviceToHost, I->stream));
+        if (mk) CK(cudaMemcpyAsync(mk, b->mk.p, bytes, cudaMemcpyDeviceToHost, I->stream));
+        if (td) CK(cudaMemcpyAsync(td, b->td.p, bytes, cudaMemcpyDeviceToHost, I->stream));
+        unsigned long long code = kNoError;
+        CK(cudaMemcpyAsync(&code, b->err.p, sizeof(code), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        if (code != kNoError) {
+            CK(cudaMemset(b->err.p, 0xFF, sizeof(unsigned long long)));
+            fail(FFSGA_ERR_CONTRACT, gene_error(code) + " (chromosome " + std::to_string(code >> 32) + ")");
+        }
+    });
+}
+
+int ffsga_cuda_batch_device_results(ffsga_cuda_batch b, const double** obj, const double** fit) {
+    return guard([&] {
+        if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        if (obj) *obj = b->obj.as<double>();
+        if (fit) *fit = b->fit.as<double>();
+    });
+}
+
+int ffsga_cuda_batch_download(ffsga_cuda_batch b, int64_t first, int64_t n, int32_t* genes) {
+    return guard([&] {
+        if (!b || !genes) fail(FFSGA_ERR_ARG, "null pointer");
+        if (first < 0 || n < 0 || first + n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_download: range");
+        auto* I = b->inst;
+        I->use();
+        const size_t L = (size_t)I->J * I->S;
+        DevBuf out;
+        out.alloc(std::max<size_t>(1, n * L * sizeof(int32_t)));
+        CK(launch_rows_to_int(I->d, b->rows.as<uint8_t>() + first * I->block(), (long long)I->block(), nullptr,
+                              out.as<int32_t>(), n, I->stream));
+        g_launches += 1;
+        CK(cudaMemcpyAsync(genes, out.p, n * L * sizeof(int32_t), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_batch_sync(ffsga_cuda_batch b) {
+    return guard([&] {
+        if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        b->inst->use();
+        CK(cudaStreamSynchronize(b->inst->stream));
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ islands
+struct ffsga_cuda_cellular_t {
+    ffsga_cuda_instance_t* inst = nullptr;
+    int n = 0, W = 0, H = 0, radius = 1, npc = 0;
+    unsigned long long gen = 0;
+    std::vector<int> slots_host;
+    DevBuf genes, sel, fit, obj, slots, st, trace, desc;
+    long long trace_cap = 0;
+    CellIsland d{};
+    int parity() const { return (int)(gen & 1ull); }
+    void push_desc() {
+        d.trace = trace.as<double>();
+        desc.ensure(sizeof(CellIsland));
+        CK(cudaMemcpy(desc.p, &d, sizeof(CellIsland), cudaMemcpyHostToDevice));
+    }
+};
+
+struct ffsga_cuda_pseudo_t {
+    ffsga_cuda_instance_t* inst = nullptr;
+    int n = 0;
+    unsigned long long gen = 0;
+    DevBuf words, fit, obj, mslot, archive, st, trace, desc;
+    long long trace_cap = 0;
+    PseudoIsland d{};
+    void push_desc() {
+        d.trace = trace.as<double>();
+        desc.ensure(sizeof(PseudoIsland));
+        CK(cudaMemcpy(desc.p, &d, sizeof(PseudoIsland), cudaMemcpyHostToDevice));
+    }
+};
+
+namespace {
+
+void neighborhood_slots(int x, int y, int w, int h, int r, std::vector<int>& out) {
+    // cellular.cpp:12-27: dy ascending, dx ascending, centre skipped, toroidal wrap
+    for (int dy = -r; dy <= r; ++dy) {
+        const int budget = r - std::abs(dy);
+        for (int dx = -budget; dx <= budget; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            const int nx = ((x + dx) % w + w) % w;
+            const int ny = ((y + dy) % h + h) % h;
+            out.push_back(ny * w + nx);
+        }
+    }
+}
+
+IslandState read_state(ffsga_cuda_instance_t* I, const DevBuf& st) {
+    IslandState s;
+    CK(cudaMemcpyAsync(&s, st.p, sizeof(s), cudaMemcpyDeviceToHost, I->stream));
+    CK(cudaStreamSynchronize(I->stream));
+    return s;
+}
+
+void refresh_stats(ffsga_cuda_cellular_t* c, ffsga_cuda_pseudo_t* p, int mode) {
+    ffsga_cuda_instance_t* I = c ? c->inst : p->inst;
+    CK(launch_island_stats(I->d, c ? c->desc.as<CellIsland>() : nullptr, c ? 1 : 0,
+                           p ? p->desc.as<PseudoIsland>() : nullptr, p ? 1 : 0, mode, I->stream));
+    g_launches += 1;
+}
+
+// storage row block of each cell in the live generation
+std::vector<long long> cell_storage_index(ffsga_cuda_cellular_t* c) {
+    std::vector<uint8_t> sel(c->n);
+    CK(cudaMemcpyAsync(sel.data(), c->sel.as<uint8_t>() + (size_t)c->parity() * c->n, c->n, cudaMemcpyDeviceToHost,
+                       c->inst->stream));
+    CK(cudaStreamSynchronize(c->inst->stream));
+    std::vector<long long> idx(c->n);
+    for (int i = 0; i < c->n; ++i) idx[i] = (long long)sel[i] * c->n + i;
+    return idx;
+}
+
+void pack_host_bits(const uint8_t* bits, int nbits, int words, std::vector<unsigned long long>& out) {
+    out.assign(words, 0ull);
+    for (int i = 0; i < nbits; ++i)
+        if (bits[i] & 1u) out[i >> 6] |= 1ull << (i & 63);
+}
+
+void unpack_host_bits(const unsigned long long* w, int nbits, uint8_t* bits) {
+    for (int i = 0; i < nbits; ++i) bits[i] = (uint8_t)((w[i >> 6] >> (i & 63)) & 1ull);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, int radius, double xr, double mr,
+                               uint64_t seed, const int32_t* init_genes, ffsga_cuda_cellular* out) {
+    return guard([&] {
+        if (!inst || !out) fail(FFSGA_ERR_ARG, "cellular_create: null pointer");
+        *out = nullptr;
+        if (width < 1 || height < 1) fail(FFSGA_ERR_CONFIG, "cellular grid shape does not match cell count");
+        if (radius < 1) fail(FFSGA_ERR_CONTRACT, "neighborhood: radius must be >= 1");
+        if (!(xr >= 0.0 && xr <= 1.0)) fail(FFSGA_ERR_CONFIG, "cellular crossover rate must lie in [0, 1]");
+        if (!(mr >= 0.0 && mr <= 1.0)) fail(FFSGA_ERR_CONFIG, "cellular mutation rate must lie in [0, 1]");
+        if ((long long)width * height > 0x3FFFFFFF) fail(FFSGA_ERR_CONFIG, "cellular island too large");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        ffsga_cuda_instance_t* I = inst;
+        auto* c = new ffsga_cuda_cellular_t();
+        std::unique_ptr<ffsga_cuda_cellular_t> hold(c);
+        c->inst = I;
+        c->W = width;
+        c->H = height;
+        c->n = width * height;
+        c->radius = radius;
+        for (int i = 0; i < c->n; ++i) neighborhood_slots(i % width, i / width, width, height, radius, c->slots_host);
+        c->npc = (int)(c->slots_host.size() / c->n);
+        upload(c->slots, c->slots_host);
+        const size_t block = I->block();
+        c->genes.alloc(2 * (size_t)c->n * block);
+        CK(cudaMemset(c->genes.p, 0, 2 * (size_t)c->n * block));
+        c->sel.alloc(2 * (size_t)c->n);
+        CK(cudaMemset(c->sel.p, 0, 2 * (size_t)c->n));
+        c->fit.alloc(2 * sizeof(double) * c->n);
+        c->obj.alloc(2 * sizeof(double) * c->n);
+        c->st.alloc(sizeof(IslandState));
+        IslandState s0{};
+        s0.arch_fit = -1.0;
+        CK(cudaMemcpy(c->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+        c->trace_cap = 1;
+        c->trace.alloc(sizeof(double));
+        if (init_genes) {
+            // explicit population (cellular.cpp:90-102), scored on the device
+            const long long L = (long long)I->J * I->S;
+            DevBuf tmp;
+            tmp.alloc(sizeof(int32_t) * L * c->n);
+            CK(cudaMemcpy(tmp.p, init_genes, sizeof(int32_t) * L * c->n, cudaMemcpyHostToDevice));
+            CK(launch_rows_from_int(I->d, tmp.as<int32_t>(), nullptr, c->genes.as<uint8_t>(), c->n, I->stream));
+            g_launches += 1;
+        } else {
+            // one sequential Rng(island_seed) stream: cell i, gene g = draw i*L + g (cellular.cpp:84-86)
+            CK(launch_random_rows(I->d, c->genes.as<uint8_t>(), (long long)block, c->n, seed, 0, false, I->stream));
+            g_launches += 1;
+        }
+        eval_rows(I, c->genes.as<uint8_t>(), c->n, c->obj.as<double>(), c->fit.as<double>(), nullptr, nullptr, true);
+        const unsigned long long code = read_error(I);
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        CellIsland& d = c->d;
+        d.n = c->n;
+        d.width = width;
+        d.height = height;
+        d.npc = c->npc;
+        d.slots = c->slots.as<int>();
+        d.genes = c->genes.as<uint8_t>();
+        d.sel = c->sel.as<uint8_t>();
+        d.fit = c->fit.as<double>();
+        d.obj = c->obj.as<double>();
+        d.seed = seed;
+        d.thr_xr = coin_threshold(xr);
+        d.thr_mu = coin_threshold(mr);
+        d.st = c->st.as<IslandState>();
+        d.item0 = 0;
+        d.cell0 = 0;
+        c->push_desc();
+        refresh_stats(c, nullptr, 0);
+        CK(cudaStreamSynchronize(I->stream));
+        *out = hold.release();
+    });
+}
+
+int ffsga_cuda_cellular_destroy(ffsga_cuda_cellular c) {
+    return guard([&] {
+        if (c) c->inst->use();
+        delete c;
+    });
+}
+
+int ffsga_cuda_cellular_size(ffsga_cuda_cellular c, int* size, int* width, int* height, int* neighbors) {
+    return guard([&] {
+        if (!c) fail(FFSGA_ERR_ARG, "null island");
+        if (size) *size = c->n;
+        if (width) *width = c->W;
+        if (height) *height = c->H;
+        if (neighbors) *neighbors = c->npc;
+    });
+}
+
+int ffsga_cuda_cellular_generation(ffsga_cuda_cellular c, uint64_t* g) {
+    return guard([&] {
+        if (!c || !g) fail(FFSGA_ERR_ARG, "null pointer");
+        *g = c->gen;
+    });
+}
+
+int ffsga_cuda_cellular_read(ffsga_cuda_cellular c, double* fit, double* obj) {
+    return guard([&] {
+        if (!c) fail(FFSGA_ERR_ARG, "null island");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        c->inst->use();
+        const size_t off = (size_t)c->parity() * c->n;
+        if (fit) CK(cudaMemcpyAsync(fit, c->fit.as<double>() + off, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->inst->stream));
+        if (obj) CK(cudaMemcpyAsync(obj, c->obj.as<double>() + off, sizeof(double) * c->n, cudaMemcpyDeviceToHost, c->inst->stream));
+        CK(cudaStreamSynchronize(c->inst->stream));
+    });
+}
+
+int ffsga_cuda_cellular_genes(ffsga_cuda_cellular c, int index, int32_t* genes) {
+    return guard([&] {
+        if (!c || !genes) fail(FFSGA_ERR_ARG, "null pointer");
+        if (index >= c->n) fail(FFSGA_ERR_CONTRACT, "cell index out of range");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        ffsga_cuda_instance_t* I = c->inst;
+        I->use();
+        std::vector<long long> idx = cell_storage_index(c);
+        if (index >= 0) idx = {idx[index]};
+        DevBuf didx, out;
+        upload(didx, idx);
+        const size_t L = (size_t)I->J * I->S;
+        out.alloc(sizeof(int32_t) * L * idx.size());
+        CK(launch_rows_to_int(I->d, c->genes.as<uint8_t>(), (long long)I->block(), didx.as<long long>(), out.as<int32_t>(),
+                              (long long)idx.size(), I->stream));
+        g_launches += 1;
+        CK(cudaMemcpyAsync(genes, out.p, sizeof(int32_t) * L * idx.size(), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_cellular_slots(ffsga_cuda_cellular c, int index, int32_t* slots) {
+    return guard([&] {
+        if (!c || !slots) fail(FFSGA_ERR_ARG, "null pointer");
+        if (index < 0 || index >= c->n) fail(FFSGA_ERR_CONTRACT, "cell index out of range");
+        for (int k = 0; k < c->npc; ++k) slots[k] = c->slots_host[(size_t)index * c->npc + k];
+    });
+}
+
+int ffsga_cuda_cellular_best(ffsga_cuda_cellular c, int* index, double* fit, double* obj) {
+    return guard([&] {
+        if (!c) fail(FFSGA_ERR_ARG, "null island");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        c->inst->use();
+        IslandState s = read_state(c->inst, c->st);
+        if (index) *index = s.best_idx;
+        if (fit) *fit = s.best_fit;
+        if (obj) *obj = s.best_obj;
+    });
+}
+
+int ffsga_cuda_cellular_install(ffsga_cuda_cellular c, int index, const int32_t* genes, double fit, double obj) {
+    return guard([&] {
+        if (!c || !genes) fail(FFSGA_ERR_ARG, "null pointer");
+        if (index < 0 || index >= c->n) fail(FFSGA_ERR_CONTRACT, "cell index out of range");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        ffsga_cuda_instance_t* I = c->inst;
+        I->use();
+        const long long slot = cell_storage_index(c)[index];
+        const size_t L = (size_t)I->J * I->S;
+        DevBuf tmp;
+        tmp.alloc(sizeof(int32_t) * L);
+        CK(cudaMemcpy(tmp.p, genes, sizeof(int32_t) * L, cudaMemcpyHostToDevice));
+        CK(launch_rows_from_int(I->d, tmp.as<int32_t>(), nullptr, c->genes.as<uint8_t>() + slot * I->block(), 1, I->stream));
+        g_launches += 1;
+        const size_t off = (size_t)c->parity() * c->n + index;
+        CK(cudaMemcpyAsync(c->fit.as<double>() + off, &fit, sizeof(double), cudaMemcpyHostToDevice, I->stream));
+        CK(cudaMemcpyAsync(c->obj.as<double>() + off, &obj, sizeof(double), cudaMemcpyHostToDevice, I->stream));
+        refresh_stats(c, nullptr, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr, uint64_t seed,
+                             ffsga_cuda_pseudo* out) {
+    return guard([&] {
+        if (!inst || !out) fail(FFSGA_ERR_ARG, "pseudo_create: null pointer");
+        *out = nullptr;
+        if (population < 2 || population % 2 != 0)
+            fail(FFSGA_ERR_CONFIG, "pseudo island population must be even and >= 2");
+        if (!(xr >= 0.0 && xr <= 1.0)) fail(FFSGA_ERR_CONFIG, "pseudo crossover rate must lie in [0, 1]");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        ffsga_cuda_instance_t* I = inst;
+        I->use();
+        auto* p = new ffsga_cuda_pseudo_t();
+        std::unique_ptr<ffsga_cuda_pseudo_t> hold(p);
+        p->inst = I;
+        p->n = population;
+        const int W = I->words;
+        p->words.alloc(sizeof(unsigned long long) * (size_t)W * population);
+        p->fit.alloc(sizeof(double) * population);
+        p->obj.alloc(sizeof(double) * population);
+        p->mslot.alloc(sizeof(long long) * population);
+        p->archive.alloc(sizeof(unsigned long long) * W);
+        CK(cudaMemset(p->archive.p, 0, sizeof(unsigned long long) * W));
+        p->st.alloc(sizeof(IslandState));
+        IslandState s0{};
+        s0.arch_fit = -1.0;  // pseudo.hpp:79
+        s0.arch_obj = 0.0;
+        CK(cudaMemcpy(p->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+        p->trace_cap = 1;
+        p->trace.alloc(sizeof(double));
+        // pairs (x, ~x): x = pair p's chromosome of the sequential init stream (pseudo.cpp:40-47)
+        const size_t block = I->block();
+        DevBuf rows;
+        rows.alloc(block * (size_t)population);
+        CK(launch_random_rows(I->d, rows.as<uint8_t>(), (long long)block, population / 2, seed, 0, false, I->stream));
+        CK(launch_pack_bits(I->d, rows.as<uint8_t>(), (long long)block, nullptr, p->words.as<unsigned long long>(), nullptr,
+                            population / 2, true, I->dBitStage.as<uint16_t>(), I->stream));
+        CK(launch_unpack_rows(I->d, p->words.as<unsigned long long>(), nullptr, rows.as<uint8_t>(), (long long)block, nullptr,
+                              population, I->stream));
+        g_launches += 3;
+        eval_rows(I, rows.as<uint8_t>(), population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, true);
+        const unsigned long long code = read_error(I);
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        PseudoIsland& d = p->d;
+        d.n = population;
+        d.words = p->words.as<unsigned long long>();
+        d.fit = p->fit.as<double>();
+        d.obj = p->obj.as<double>();
+        d.mslot = p->mslot.as<long long>();
+        d.archive = p->archive.as<unsigned long long>();
+        d.seed = seed;
+        d.thr_xr = coin_threshold(xr);
+        d.st = p->st.as<IslandState>();
+        d.pair0 = 0;
+        p->push_desc();
+        refresh_stats(nullptr, p, 2);  // archive = first max over the scored members
+        CK(cudaStreamSynchronize(I->stream));
+        *out = hold.release();
+    });
+}
+
+int ffsga_cuda_pseudo_destroy(ffsga_cuda_pseudo p) {
+    return guard([&] {
+        if (p) p->inst->use();
+        delete p;
+    });
+}
+
+int ffsga_cuda_pseudo_size(ffsga_cuda_pseudo p, int* size, int* total_bits) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "null island");
+        if (size) *size = p->n;
+        if (total_bits) *total_bits = p->inst->total_bits;
+    });
+}
+
+int ffsga_cuda_pseudo_generation(ffsga_cuda_pseudo p, uint64_t* g) {
+    return guard([&] {
+        if (!p || !g) fail(FFSGA_ERR_ARG, "null pointer");
+        *g = p->gen;
+    });
+}
+
+int ffsga_cuda_pseudo_read(ffsga_cuda_pseudo p, double* fit, double* obj) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "null island");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        p->inst->use();
+        if (fit) CK(cudaMemcpyAsync(fit, p->fit.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->inst->stream));
+        if (obj) CK(cudaMemcpyAsync(obj, p->obj.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->inst->stream));
+        CK(cudaStreamSynchronize(p->inst->stream));
+    });
+}
+
+int ffsga_cuda_pseudo_member(ffsga_cuda_pseudo p, int index, uint8_t* bits) {
+    return guard([&] {
+        if (!p || !bits) fail(FFSGA_ERR_ARG, "null pointer");
+        if (index >= p->n) fail(FFSGA_ERR_CONTRACT, "member index out of range");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        ffsga_cuda_instance_t* I = p->inst;
+        I->use();
+        const int W = I->words, nb = I->total_bits;
+        const int first = index < 0 ? 0 : index;
+        const int count = index < 0 ? p->n : 1;
+        std::vector<unsigned long long> w((size_t)W * count);
+        CK(cudaMemcpyAsync(w.data(), p->words.as<unsigned long long>() + (size_t)first * W, sizeof(unsigned long long) * w.size(),
+                           cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        for (int i = 0; i < count; ++i) unpack_host_bits(w.data() + (size_t)i * W, nb, bits + (size_t)i * nb);
+    });
+}
+
+int ffsga_cuda_pseudo_best(ffsga_cuda_pseudo p, int* index, double* fit, double* obj) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "null island");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        p->inst->use();
+        IslandState s = read_state(p->inst, p->st);
+        if (index) *index = s.best_idx;
+        if (fit) *fit = s.best_fit;
+        if (obj) *obj = s.best_obj;
+    });
+}
+
+int ffsga_cuda_pseudo_archive(ffsga_cuda_pseudo p, double* fit, double* obj, uint8_t* bits) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "null island");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        ffsga_cuda_instance_t* I = p->inst;
+        I->use();
+        IslandState s = read_state(I, p->st);
+        if (fit) *fit = s.arch_fit;
+        if (obj) *obj = s.arch_obj;
+        if (bits) {
+            std::vector<unsigned long long> w(I->words);
+            CK(cudaMemcpy(w.data(), p->archive.p, sizeof(unsigned long long) * I->words, cudaMemcpyDeviceToHost));
+            unpack_host_bits(w.data(), I->total_bits, bits);
+        }
+    });
+}
+
+int ffsga_cuda_pseudo_install(ffsga_cuda_pseudo p, int index, const uint8_t* bits, double fit, double obj) {
+    return guard([&] {
+        if (!p || !bits) fail(FFSGA_ERR_ARG, "null pointer");
+        if (index < 0 || index >= p->n) fail(FFSGA_ERR_CONTRACT, "member index out of range");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        ffsga_cuda_instance_t* I = p->inst;
+        I->use();
+        std::vector<unsigned long long> w;
+        pack_host_bits(bits, I->total_bits, I->words, w);
+        CK(cudaMemcpy(p->words.as<unsigned long long>() + (size_t)index * I->words, w.data(),
+                      sizeof(unsigned long long) * I->words, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->fit.as<double>() + index, &fit, sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->obj.as<double>() + index, &obj, sizeof(double), cudaMemcpyHostToDevice));
+        IslandState s = read_state(I, p->st);
+        if (fit > s.arch_fit) {  // consider_for_archive (pseudo.cpp:106-113)
+            s.arch_fit = fit;
+            s.arch_obj = obj;
+            CK(cudaMemcpy(p->st.p, &s, sizeof(s), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(p->archive.p, w.data(), sizeof(unsigned long long) * I->words, cudaMemcpyHostToDevice));
+        }
+        refresh_stats(nullptr, p, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_pseudo* pseudos, int np,
+                    int generations, double* trace_c, double* trace_p) {
+    return guard([&] {
+        if (nc < 0 || np < 0 || (nc > 0 && !cells) || (np > 0 && !pseudos)) fail(FFSGA_ERR_ARG, "step: bad island list");
+        if (generations < 0) fail(FFSGA_ERR_CONTRACT, "step: negative generation count");
+        if (nc + np == 0 || generations == 0) return;
+        ffsga_cuda_instance_t* I = nc > 0 ? cells[0]->inst : pseudos[0]->inst;
+        for (int i = 0; i < nc; ++i)
+            if (!cells[i] || cells[i]->inst != I) fail(FFSGA_ERR_ARG, "step: islands must share one instance");
+        for (int i = 0; i < np; ++i)
+            if (!pseudos[i] || pseudos[i]->inst != I) fail(FFSGA_ERR_ARG, "step: islands must share one instance");
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        // descriptors of this joint step: work items = every cell, then crossed pseudo members
+        std::vector<CellIsland> cd(nc);
+        std::vector<PseudoIsland> pd(np);
+        long long n_cells = 0, n_pairs = 0;
+        for (int i = 0; i < nc; ++i) {
+            auto* c = cells[i];
+            if (c->trace_cap < generations) {
+                c->trace.alloc(sizeof(double) * generations);
+                c->trace_cap = generations;
+            }
+            c->d.trace = c->trace.as<double>();
+            cd[i] = c->d;
+            cd[i].item0 = n_cells;
+            cd[i].cell0 = n_cells;
+            n_cells += c->n;
+            CK(cudaMemcpyAsync(&c->st.as<IslandState>()->seg_start, &c->gen, sizeof(unsigned long long),
+                               cudaMemcpyHostToDevice, I->stream));
+        }
+        for (int i = 0; i < np; ++i) {
+            auto* p = pseudos[i];
+            if (p->trace_cap < generations) {
+                p->trace.alloc(sizeof(double) * generations);
+                p->trace_cap = generations;
+            }
+            p->d.trace = p->trace.as<double>();
+            pd[i] = p->d;
+            pd[i].pair0 = n_pairs;
+            n_pairs += p->n / 2;
+            CK(cudaMemcpyAsync(&p->st.as<IslandState>()->seg_start, &p->gen, sizeof(unsigned long long),
+                               cudaMemcpyHostToDevice, I->stream));
+        }
+        const long long cap = n_cells + 2 * n_pairs;
+        I->wl_ptrs.ensure(sizeof(void*) * cap);
+        I->wl_obj.ensure(sizeof(double) * cap);
+        I->wl_fit.ensure(sizeof(double) * cap);
+        I->wl_scratch.ensure(std::max<size_t>(1, (size_t)(2 * n_pairs) * I->block()));
+        I->cell_desc.ensure(sizeof(CellIsland) * std::max(1, nc));
+        I->pseudo_desc.ensure(sizeof(PseudoIsland) * std::max(1, np));
+        if (nc) CK(cudaMemcpyAsync(I->cell_desc.p, cd.data(), sizeof(CellIsland) * nc, cudaMemcpyHostToDevice, I->stream));
+        if (np) CK(cudaMemcpyAsync(I->pseudo_desc.p, pd.data(), sizeof(PseudoIsland) * np, cudaMemcpyHostToDevice, I->stream));
+        WorkList wl{};
+        wl.ptrs = I->wl_ptrs.as<const uint8_t*>();
+        wl.obj = I->wl_obj.as<double>();
+        wl.fit = I->wl_fit.as<double>();
+        wl.count = I->wl_count.as<long long>();
+        wl.scratch = I->wl_scratch.as<uint8_t>();
+        wl.scratch0 = n_cells;
+        const CellIsland* cdev = I->cell_desc.as<CellIsland>();
+        const PseudoIsland* pdev = I->pseudo_desc.as<PseudoIsland>();
+        EvalItems W{};
+        W.n_dev = wl.count;
+        W.ptrs = wl.ptrs;
+        W.obj = wl.obj;
+        W.fit = wl.fit;
+        for (int g = 0; g < generations; ++g) {
+            I->timed(1, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, pdev, np, n_pairs, wl, I->stream)); });
+            I->timed(0, [&] { CK(launch_eval(I->d, I->ec, W, cap, I->sm_count, false, I->stream)); });
+            I->timed(2, [&] { CK(launch_commit(I->d, cdev, nc, pdev, np, wl, I->stream)); });
+            g_launches += 3 + (nc > 0 ? 1 : 0) + (np > 0 ? 1 : 0);
+        }
+        for (int i = 0; i < nc; ++i) {
+            if (trace_c)
+                CK(cudaMemcpyAsync(trace_c + (size_t)i * generations, cells[i]->trace.p, sizeof(double) * generations,
+                                   cudaMemcpyDeviceToHost, I->stream));
+        }
+        for (int i = 0; i < np; ++i) {
+            if (trace_p)
+                CK(cudaMemcpyAsync(trace_p + (size_t)i * generations, pseudos[i]->trace.p, sizeof(double) * generations,
+                                   cudaMemcpyDeviceToHost, I->stream));
+        }
+        CK(cudaStreamSynchronize(I->stream));
+        for (int i = 0; i < nc; ++i) cells[i]->gen += (unsigned long long)generations;
+        for (int i = 0; i < np; ++i) pseudos[i]->gen += (unsigned long long)generations;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// sort_island order (fitness desc, index asc) of n fitness values into idx_out (device)
+void sort_island_dev(ffsga_cuda_instance_t* I, const double* fit, long long n, DevBuf& idx_out) {
+    I->mg_keys0.ensure(sizeof(double) * n);
+    I->mg_keys1.ensure(sizeof(double) * n);
+    I->mg_idx0.ensure(sizeof(long long) * n);
+    idx_out.ensure(sizeof(long long) * n);
+    const size_t tb = sort_temp_bytes(n);
+    I->mg_temp.ensure(std::max<size_t>(tb, 16));
+    CK(launch_sort_desc(fit, n, I->mg_keys0.as<double>(), I->mg_keys1.as<double>(), I->mg_idx0.as<long long>(),
+                        idx_out.as<long long>(), I->mg_temp.p, tb, I->stream));
+    g_launches += 3;
+}
+
+void check_count(int k, int a, int b) {  // migration.cpp:40-43
+    if (k < 0 || k > a || k > b) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffsga_cuda_migrate_cellular_to_pseudo(ffsga_cuda_cellular from, ffsga_cuda_pseudo to, int k) {
+    return guard([&] {
+        if (!from || !to) fail(FFSGA_ERR_ARG, "migrate: null island");
+        if (from->inst != to->inst) fail(FFSGA_ERR_ARG, "migrate: islands must share one instance");
+        check_count(k, from->n, to->n);
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = from->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        const int q = from->parity();
+        sort_island_dev(I, from->fit.as<double>() + (size_t)q * from->n, from->n, I->mg_idx_a);
+        sort_island_dev(I, to->fit.as<double>(), to->n, I->mg_idx_b);
+        CK(launch_migrate_c2p(I->d, from->d, to->d, I->mg_idx_a.as<long long>(), I->mg_idx_b.as<long long>(), k, q,
+                              I->dBitStage.as<uint16_t>(), I->stream));
+        g_launches += 2;
+        refresh_stats(nullptr, to, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_migrate_pseudo_to_cellular(ffsga_cuda_pseudo from, ffsga_cuda_cellular to, int k) {
+    return guard([&] {
+        if (!from || !to) fail(FFSGA_ERR_ARG, "migrate: null island");
+        if (from->inst != to->inst) fail(FFSGA_ERR_ARG, "migrate: islands must share one instance");
+        check_count(k, from->n, to->n);
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = from->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        const int q = to->parity();
+        sort_island_dev(I, from->fit.as<double>(), from->n, I->mg_idx_a);
+        sort_island_dev(I, to->fit.as<double>() + (size_t)q * to->n, to->n, I->mg_idx_b);
+        CK(launch_migrate_p2c(I->d, from->d, to->d, I->mg_idx_a.as<long long>(), I->mg_idx_b.as<long long>(), k, q,
+                              I->stream));
+        g_launches += 1;
+        refresh_stats(to, nullptr, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_set_timing(ffsga_cuda_instance inst, int enabled) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        inst->timing = enabled != 0;
+    });
+}
+
+int ffsga_cuda_timing(ffsga_cuda_instance inst, int which, double* ms, int64_t* launches) {
+    return guard([&] {
+        if (!inst || which < 0 || which > 2) fail(FFSGA_ERR_ARG, "timing: bad argument");
+        if (ms) *ms = inst->t_ms[which];
+        if (launches) *launches = inst->t_n[which];
+    });
+}
+
+int ffsga_cuda_reset_timing(ffsga_cuda_instance inst) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        for (int i = 0; i < 3; ++i) {
+            inst->t_ms[i] = 0;
+            inst->t_n[i] = 0;
+        }
+    });
+}
+
+int ffsga_cuda_launch_count(int64_t* count) {
+    return guard([&] {
+        if (!count) fail(FFSGA_ERR_ARG, "null pointer");
+        *count = g_launches.load();
+    });
+}
+
+}  // extern "C"

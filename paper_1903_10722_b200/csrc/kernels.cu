@@ -1,0 +1,1002 @@
+// kernels.cu -- sm_100a kernels of the FFS hot path.
+//
+//   K1  k_eval            decode + evaluate a batch (Evaluator::score, model.cpp:61-120,183-195)
+//   K2  k_random_rows     random assignment chromosomes (chromosome.cpp:68-74)
+//   K3  k_cell_breed      cellular selection / two-point crossover / mutation (cellular.cpp:108-150)
+//   K4  k_pseudo_breed    complementary-pair mask crossover (pseudo.cpp:11-29,59-82)
+//   K6  k_commit          replacement, archive, best index, trace (cellular.cpp:164-189,
+//                         pseudo.cpp:83-96, solver.cpp:111-123)
+//   K5  migration         sort_island order + install with representation change (migration.cpp:47-69)
+//   K7  k_eval<SCHED>     full timetable of one chromosome (model.cpp:124-139)
+//
+// All fp64 arithmetic uses explicit round-to-nearest intrinsics (no FMA contraction) so results
+// are bit-identical to the reference built with -ffp-contract=off (proj/src/CMakeLists.txt:16).
+#include <cub/cub.cuh>
+
+#include "launch.h"
+
+namespace ffsga_dev {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000LL); }
+
+template <int G>
+__device__ __forceinline__ double group_max(double v) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        double o = __shfl_xor_sync(kFull, v, off, G);
+        v = (v < o) ? o : v;
+    }
+    return v;
+}
+
+template <int G>
+__device__ __forceinline__ int group_min_int(int v) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) v = min(v, __shfl_xor_sync(kFull, v, off, G));
+    return v;
+}
+
+template <int G>
+__device__ __forceinline__ void group_min_key(double& c, int& j) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        double oc = __shfl_xor_sync(kFull, c, off, G);
+        int oj = __shfl_xor_sync(kFull, j, off, G);
+        if (oc < c || (oc == c && oj < j)) { c = oc; j = oj; }
+    }
+}
+
+// ---------------------------------------------------------------------------- K1 decoder
+// One stage of the list schedule for the group's chromosome (model.cpp:68-95).
+// Lane m (< Ms) merges the NS incoming per-source linked lists of jobs routed to machine m
+// (each list is sorted by completion because completions on one machine strictly increase),
+// which reproduces the (ready, job) sort of model.cpp:72-75 restricted to machine m, then runs
+// the machine's fp64 recurrence start = max(ready, avail), completion = start + p (84-87).
+// Each dispatched job is appended to the outgoing list (m -> gene of the next stage).
+template <int G, int NS, bool SCHED>
+__device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
+                                           int m, bool work, double* __restrict__ ready,
+                                           uint16_t* __restrict__ nxt, uint16_t* __restrict__ tail,
+                                           const uint8_t* __restrict__ row, BadTrack& bad,
+                                           const EvalItems& W) {
+    const int J = I.J;
+    const int END = J;
+    const bool last = (Mnext == 0);
+    const double* pcol = I.procT + (size_t)(I.stage_off[s] + (m < Ms ? m : 0)) * (J + 1);
+    double hr[NS], hp[NS];
+    int hj[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        int j = (work && m < Ms && k < Mprev) ? (int)nxt[J + 1 + k * G + m] : END;
+        hj[k] = j;
+        hr[k] = ready[j];
+        hp[k] = __ldg(pcol + j);
+    }
+    uint16_t* mytail = tail + m * G;
+    if (!last) {
+#pragma unroll
+        for (int d = 0; d < G; ++d) mytail[d] = (uint16_t)(J + 1 + m * G + d);
+    }
+    __syncwarp();
+    if (work && m < Ms) {
+        double avail = 0.0;
+        while (true) {
+            int bs = 0;
+            double br = hr[0], bp = hp[0];
+            int bj = hj[0];
+#pragma unroll
+            for (int k = 1; k < NS; ++k) {
+                bool lt = (hr[k] < br) || (hr[k] == br && hj[k] < bj);
+                br = lt ? hr[k] : br;
+                bp = lt ? hp[k] : bp;
+                bj = lt ? hj[k] : bj;
+                bs = lt ? k : bs;
+            }
+            if (bj == END) break;
+            const int nh = nxt[bj];
+            const double nr = ready[nh];
+            const double np = __ldg(pcol + nh);
+            const double start = (br < avail) ? avail : br;  // std::max(ready, avail)
+            const double c = __dadd_rn(start, bp);
+            avail = c;
+            ready[bj] = c;
+            if (SCHED) {
+                const int at = bj * I.S + s;
+                W.smachine[at] = m;
+                W.sstart[at] = start;
+                W.scomp[at] = c;
+            }
+            if (!last) {
+                const int d = row[bj];
+                if (d < Mnext) {
+                    const int t = mytail[d];
+                    nxt[t] = (uint16_t)bj;
+                    mytail[d] = (uint16_t)bj;
+                } else {
+                    bad.consider(c, bj);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (k == bs) {
+                    hj[k] = nh;
+                    hr[k] = nr;
+                    hp[k] = np;
+                }
+        }
+        if (!last) {
+#pragma unroll
+            for (int d = 0; d < G; ++d) nxt[mytail[d]] = (uint16_t)END;
+        }
+    }
+    __syncwarp();
+}
+
+template <int G, bool SCHED>
+__device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
+                                               int m, bool work, double* ready, uint16_t* nxt,
+                                               uint16_t* tail, const uint8_t* row, BadTrack& bad,
+                                               const EvalItems& W) {
+#define FFSGA_STAGE(NS_)                                                                        \
+    if constexpr (NS_ <= G) {                                                                    \
+        if (Mprev <= NS_) {                                                                      \
+            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row,    \
+                                      bad, W);                                                   \
+            return;                                                                              \
+        }                                                                                        \
+    }
+    FFSGA_STAGE(1)
+    FFSGA_STAGE(2)
+    FFSGA_STAGE(3)
+    FFSGA_STAGE(4)
+    FFSGA_STAGE(5)
+    FFSGA_STAGE(6)
+    FFSGA_STAGE(7)
+    FFSGA_STAGE(8)
+    FFSGA_STAGE(16)
+    FFSGA_STAGE(32)
+#undef FFSGA_STAGE
+}
+
+template <int G>
+__device__ __forceinline__ void load_row(const DevInst& I, const uint8_t* genes, int s, int m,
+                                         uint8_t* row) {
+    const uint4* src = reinterpret_cast<const uint4*>(genes + (size_t)s * I.Jpad);
+    uint4* dst = reinterpret_cast<uint4*>(row);
+    for (int v = m; v < I.Jpad / 16; v += G) dst[v] = __ldg(src + v);
+}
+
+template <int G, bool SCHED>
+__global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int gw = lane / G;
+    const int m = lane % G;
+    const int gid = threadIdx.x / G;
+    unsigned char* gb = smem + (size_t)gid * GL.bytes;
+    double* ready = reinterpret_cast<double*>(gb);
+    uint16_t* nxt = reinterpret_cast<uint16_t*>(gb + GL.off_next);
+    uint16_t* tail = reinterpret_cast<uint16_t*>(gb + GL.off_tail);
+    uint8_t* row = gb + GL.off_row;
+    const int J = I.J, S = I.S;
+    const int END = J;
+    const long long n = W.n_dev ? *W.n_dev : W.n;
+
+    for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
+         base += (long long)gridDim.x * groups_per_cta) {
+        const long long item = base + gid;
+        const bool active = item < n;
+        if (__all_sync(kFull, !active)) continue;
+        const uint8_t* genes = nullptr;
+        if (active) genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
+
+        // ---- init: ready = release, END sentinel = +inf; stage-0 gene row
+        if (active) {
+            for (int j = m; j < J; j += G) ready[j] = __ldg(I.release + j);
+            if (m == 0) ready[END] = dinf();
+            load_row<G>(I, genes, 0, m, row);
+        }
+        tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
+        __syncwarp();
+
+        // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order.
+        // A chunk of G consecutive release-order jobs is linked with one match_any per chunk.
+        const int M0 = I.M[0];
+        int bad_k = 0x7FFFFFFF;
+        for (int b0 = 0; b0 < J; b0 += G) {
+            const int k = b0 + m;
+            const bool valid = active && k < J;
+            const int j = valid ? (int)I.rel_order[k] : 0;
+            const int d = valid ? (int)row[j] : 0;
+            const bool good = valid && d < M0;
+            if (valid && !good) bad_k = min(bad_k, k);
+            const unsigned key = good ? (((unsigned)gw << 8) | (unsigned)d) : (0x10000u | (unsigned)lane);
+            const unsigned peers = __match_any_sync(kFull, key);
+            const unsigned below = peers & ((1u << lane) - 1u);
+            const unsigned above = peers & ~((2u << lane) - 1u);
+            const int pred_lane = below ? (31 - __clz(below)) : lane;
+            const int pred_j = __shfl_sync(kFull, j, pred_lane);
+            int t = 0;
+            if (good && !below) t = tail[d];
+            __syncwarp();
+            if (good) nxt[below ? pred_j : t] = (uint16_t)j;
+            if (good && !above) tail[d] = (uint16_t)j;
+            __syncwarp();
+        }
+        if (active) nxt[tail[m]] = (uint16_t)END;
+        bad_k = group_min_int<G>(bad_k);
+        bool work = active;
+        if (active && bad_k != 0x7FFFFFFF) {
+            work = false;
+            if (m == 0 && W.err)
+                atomicMin(W.err, ((unsigned long long)item << 32) | (0ull << 16) |
+                                     (unsigned long long)I.rel_order[bad_k]);
+        }
+        __syncwarp();
+
+        // ---- stages
+        int Mprev = 1;
+        for (int s = 0; s < S; ++s) {
+            const int Ms = I.M[s];
+            const int Mnext = (s + 1 < S) ? I.M[s + 1] : 0;
+            if (work && Mnext) load_row<G>(I, genes, s + 1, m, row);
+            BadTrack bad;
+            bad.reset();
+            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, bad, W);
+            if (Mnext) {
+                double bc = bad.c;
+                int bj = bad.j;
+                group_min_key<G>(bc, bj);
+                if (work && bj != 0x7FFFFFFF) {
+                    work = false;
+                    if (m == 0 && W.err)
+                        atomicMin(W.err, ((unsigned long long)item << 32) |
+                                             ((unsigned long long)(s + 1) << 16) | (unsigned long long)bj);
+                }
+            }
+            Mprev = Ms;
+        }
+
+        // ---- report_from_completions (model.cpp:107-120)
+        double mk = 0.0;
+        if (work) {
+            for (int j = m; j < J; j += G) {
+                const double c = ready[j];
+                mk = (mk < c) ? c : mk;
+                const double t = __dsub_rn(c, __ldg(I.due + j));
+                ready[j] = (0.0 < t) ? t : 0.0;  // std::max(0.0, c - due)
+            }
+        }
+        mk = group_max<G>(mk);
+        __syncwarp();
+        if (work && m == 0) {
+            double T = 0.0;  // sequential in job order: the fp64 sum is order dependent
+            for (int j = 0; j < J; ++j) T = __dadd_rn(T, ready[j]);
+            const double obj = __dadd_rn(__dmul_rn(I.weight, T), mk);
+            const double f = __dsub_rn(I.emax, obj);
+            W.obj[item] = obj;
+            W.fit[item] = (f < 0.0) ? 0.0 : f;  // std::max(emax - obj, 0.0)
+            if (W.mk) W.mk[item] = mk;
+            if (W.td) W.td[item] = T;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------- K2 random rows
+__global__ void __launch_bounds__(256) k_random_rows(DevInst I, uint8_t* out, long long stride, long long n,
+                                                      unsigned long long base, long long first, int per_item) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const long long item = warp;
+    const unsigned long long seed = per_item ? derive_seed(base, (unsigned long long)(first + item)) : base;
+    const unsigned long long off = per_item ? 0ull : (unsigned long long)(first + item) * (unsigned long long)(I.J * I.S);
+    uint8_t* dst = out + item * stride;
+    const int words_per_row = I.Jpad / 4;
+    for (int w = lane; w < I.S * words_per_row; w += 32) {
+        const int s = w / words_per_row;
+        const int j0 = (w % words_per_row) * 4;
+        const int Ms = I.M[s];
+        unsigned v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = j0 + b;
+            if (j < I.J) {
+                const unsigned g = (unsigned)index_of(draw(seed, off + (unsigned long long)(j * I.S + s)), Ms);
+                v |= g << (8 * b);
+            }
+        }
+        reinterpret_cast<unsigned*>(dst + (size_t)s * I.Jpad)[j0 / 4] = v;
+    }
+}
+
+// int32 / uint8 job-major host layout -> device stage-major rows (255 marks out-of-range genes)
+__global__ void __launch_bounds__(256) k_rows_from_int(DevInst I, const int32_t* gi, const uint8_t* gu,
+                                                        uint8_t* rows, long long n) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const long long L = (long long)I.J * I.S;
+    uint8_t* dst = rows + warp * (long long)I.S * I.Jpad;
+    for (int idx = lane; idx < I.S * I.Jpad; idx += 32) {
+        const int s = idx / I.Jpad, j = idx % I.Jpad;
+        uint8_t v = 0;
+        if (j < I.J) {
+            if (gi) {
+                const int32_t x = gi[warp * L + (long long)j * I.S + s];
+                v = (x < 0 || x > 254) ? (uint8_t)255 : (uint8_t)x;
+            } else {
+                v = gu[warp * L + (long long)j * I.S + s];
+            }
+        }
+        dst[idx] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rows_to_int(DevInst I, const uint8_t* rows, long long row_stride,
+                                                      const long long* src_idx, int32_t* out, long long n) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const long long src = src_idx ? src_idx[warp] : warp;
+    const uint8_t* r = rows + src * row_stride;
+    const long long L = (long long)I.J * I.S;
+    for (int g = lane; g < L; g += 32) {
+        const int j = g / I.S, s = g % I.S;
+        out[warp * L + g] = r[(size_t)s * I.Jpad + j];
+    }
+}
+
+// ---------------------------------------------------------------------------- bit views
+// int_to_bits (chromosome.cpp:28-42): gene (j,s) -> bits_per_stage[s] slot at j*bpj + sbo[s],
+// MSB first.  bit_stage[r] = stage owning bit r of a job.  Packed LSB-first in u64 words.
+__device__ __forceinline__ unsigned long long pack_word(const DevInst& I, const uint8_t* r, int w,
+                                                         const uint16_t* bit_stage) {
+    unsigned long long out = 0;
+    const int b0 = w * 64;
+    const int b1 = min(b0 + 64, I.total_bits);
+    int job = b0 / I.bits_per_job;
+    int rr = b0 - job * I.bits_per_job;
+    for (int b = b0; b < b1; ++b) {
+        const int s = bit_stage[rr];
+        const int pos = rr - I.sbo[s];
+        const int nb = I.bps[s];
+        const unsigned v = r[(size_t)s * I.Jpad + job];
+        out |= (unsigned long long)((v >> (nb - 1 - pos)) & 1u) << (b - b0);
+        if (++rr == I.bits_per_job) { rr = 0; ++job; }
+    }
+    return out;
+}
+
+__global__ void __launch_bounds__(256) k_pack_bits(DevInst I, const uint8_t* rows, long long row_stride,
+                                                    const long long* src_idx, unsigned long long* words,
+                                                    const long long* dst_idx, long long n, int with_complement,
+                                                    const uint16_t* bit_stage) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const long long src = src_idx ? src_idx[warp] : warp;
+    const long long dst = dst_idx ? dst_idx[warp] : warp;
+    const uint8_t* r = rows + src * row_stride;
+    for (int w = lane; w < I.words; w += 32) {
+        const unsigned long long x = pack_word(I, r, w, bit_stage);
+        if (with_complement) {
+            const int nb = min(64, I.total_bits - w * 64);
+            const unsigned long long valid = nb == 64 ? ~0ull : ((1ull << nb) - 1ull);
+            words[(2 * dst) * I.words + w] = x;
+            words[(2 * dst + 1) * I.words + w] = (~x) & valid;  // complement (chromosome.cpp:61-66)
+        } else {
+            words[dst * I.words + w] = x;
+        }
+    }
+}
+
+// bits_to_int (chromosome.cpp:44-59): slot value MSB-first, modulo the stage's machines.
+__device__ __forceinline__ unsigned extract_gene(const DevInst& I, const unsigned long long* wv, int j, int s) {
+    const int o = j * I.bits_per_job + I.sbo[s];
+    const int nb = I.bps[s];
+    const int w = o >> 6, sh = o & 63;
+    unsigned long long x = wv[w] >> sh;
+    if (sh + nb > 64) x |= wv[w + 1] << (64 - sh);
+    const unsigned raw = (unsigned)(x & ((1ull << nb) - 1ull));  // bit o at position 0
+    const unsigned val = __brev(raw) >> (32 - nb);               // bit o becomes the MSB
+    return val % (unsigned)I.M[s];
+}
+
+__device__ __forceinline__ void unpack_member(const DevInst& I, const unsigned long long* wv, uint8_t* dst,
+                                              int lane) {
+    const int words_per_row = I.Jpad / 4;
+    for (int w = lane; w < I.S * words_per_row; w += 32) {
+        const int s = w / words_per_row;
+        const int j0 = (w % words_per_row) * 4;
+        unsigned v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            if (j0 + b < I.J) v |= extract_gene(I, wv, j0 + b, s) << (8 * b);
+        reinterpret_cast<unsigned*>(dst + (size_t)s * I.Jpad)[j0 / 4] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_unpack_rows(DevInst I, const unsigned long long* words,
+                                                      const long long* src_idx, uint8_t* rows, long long row_stride,
+                                                      const long long* dst_idx, long long n) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const long long src = src_idx ? src_idx[warp] : warp;
+    const long long dst = dst_idx ? dst_idx[warp] : warp;
+    unpack_member(I, words + src * I.words, rows + dst * row_stride, lane);
+}
+
+// ---------------------------------------------------------------------------- K3 cellular breed
+constexpr int kMutChunk = 8;  // draws per lane per window of the mutation stream parse
+
+// compute_cell (cellular.cpp:116-150) for one cell per warp.  The serial prefix (tournaments,
+// crossover coin and cut points) is replayed redundantly by every lane; the mutation loop
+// (one coin per gene plus one index draw per mutated gene, 148-150) is parsed warp-parallel:
+// draw k of the cell stream is mix(seed + (k+1) gamma), so each lane evaluates its slice of
+// the stream and a warp scan of the 2-state {coin, index} automaton assigns gene indices.
+__global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland* __restrict__ isl,
+                                                     int n_islands, long long n_cells, WorkList wl) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_cells) return;
+    int ii = 0;
+    while (ii + 1 < n_islands && isl[ii + 1].cell0 <= warp) ++ii;
+    const CellIsland& C = isl[ii];
+    const int cell = (int)(warp - C.cell0);
+    const int n = C.n;
+    const unsigned long long gen = C.st->gen;
+    const int q = (int)(gen & 1ull);
+    const double* fit = C.fit + (size_t)q * n;
+    const uint8_t* selq = C.sel + (size_t)q * n;
+    const unsigned long long gen_seed = derive_seed(C.seed, gen + 1ull);  // cellular.cpp:167
+    const unsigned long long cs = derive_seed(gen_seed, (unsigned long long)cell);  // :171
+    const int L = I.J * I.S;
+    unsigned long long k = 0;
+    const int npc = C.npc;
+    const int* slots = C.slots + (size_t)cell * npc;
+
+    auto tour = [&]() {  // cellular.cpp:108-112
+        const int a = slots[index_of(draw(cs, k), npc)];
+        const int b = slots[index_of(draw(cs, k + 1), npc)];
+        k += 2;
+        return fit[b] > fit[a] ? b : a;
+    };
+    const int p1 = tour();
+    int p2 = tour();
+    for (int tries = 0; p2 == p1 && tries < 8; ++tries) p2 = tour();
+    if (p2 == p1) {
+        for (int t = 0; t < npc; ++t)
+            if (slots[t] != p1) { p2 = slots[t]; break; }
+    }
+    const bool crossed = coin_of(draw(cs, k++), C.thr_xr);
+    int lo = 0, hi = 0;
+    if (crossed) {
+        const int a = index_of(draw(cs, k++), L + 1);
+        int b = index_of(draw(cs, k++), L + 1);
+        while (b == a) b = index_of(draw(cs, k++), L + 1);
+        lo = min(a, b);
+        hi = max(a, b);
+    }
+
+    const size_t block = (size_t)I.S * I.Jpad;
+    const uint8_t* g1 = C.genes + ((size_t)selq[p1] * n + p1) * block;
+    const uint8_t* g2 = C.genes + ((size_t)selq[p2] * n + p2) * block;
+    uint8_t* child = C.genes + ((size_t)(1 - selq[cell]) * n + cell) * block;
+
+    // two-point crossover on the job-major index i = j*S + s (cellular.cpp:136-146)
+    const int vec_per_row = I.Jpad / 16;
+    for (int v = lane; v < I.S * vec_per_row; v += 32) {
+        const int s = v / vec_per_row;
+        const int j0 = (v % vec_per_row) * 16;
+        uint4 a = __ldg(reinterpret_cast<const uint4*>(g1 + (size_t)s * I.Jpad) + (j0 / 16));
+        if (crossed) {
+            // jobs with lo <= j*S+s < hi take parent 2
+            const int jlo = lo - s <= 0 ? 0 : (lo - s + I.S - 1) / I.S;
+            const int jhi = hi - s <= 0 ? 0 : (hi - s + I.S - 1) / I.S;
+            if (jlo < j0 + 16 && jhi > j0 && jlo < jhi) {
+                const uint4 b = __ldg(reinterpret_cast<const uint4*>(g2 + (size_t)s * I.Jpad) + (j0 / 16));
+                unsigned* pa = reinterpret_cast<unsigned*>(&a);
+                const unsigned* pb = reinterpret_cast<const unsigned*>(&b);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    unsigned msk = 0;
+#pragma unroll
+                    for (int by = 0; by < 4; ++by) {
+                        const int j = j0 + 4 * w + by;
+                        if (j >= jlo && j < jhi) msk |= 0xFFu << (8 * by);
+                    }
+                    pa[w] = (pa[w] & ~msk) | (pb[w] & msk);
+                }
+            }
+        }
+        reinterpret_cast<uint4*>(child + (size_t)s * I.Jpad)[j0 / 16] = a;
+    }
+    __syncwarp();
+
+    // mutation (cellular.cpp:148-150)
+    const unsigned long long thr = C.thr_mu;
+    unsigned long long pos = k;
+    long long coins_before = 0;
+    bool st_coin = true;
+    while (coins_before < L || (coins_before == L && !st_coin)) {
+        unsigned long long u[kMutChunk];
+        unsigned tb = 0;
+        const unsigned long long p0 = pos + (unsigned long long)lane * kMutChunk;
+#pragma unroll
+        for (int t = 0; t < kMutChunk; ++t) {
+            u[t] = draw(cs, p0 + t);
+            tb |= (coin_of(u[t], thr) ? 1u : 0u) << t;
+        }
+        // transfer function of this lane's slice for both entry states
+        int f1 = 1, c1 = 0, f0 = 0, c0 = 0;
+#pragma unroll
+        for (int t = 0; t < kMutChunk; ++t) {
+            const int bit = (tb >> t) & 1;
+            if (f1) { ++c1; f1 = !bit; } else { f1 = 1; }
+            if (f0) { ++c0; f0 = !bit; } else { f0 = 1; }
+        }
+        // inclusive scan (composition) over lanes
+        int F0 = f0, F1 = f1, C0 = c0, C1 = c1;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int pF0 = __shfl_up_sync(kFull, F0, off);
+            const int pF1 = __shfl_up_sync(kFull, F1, off);
+            const int pC0 = __shfl_up_sync(kFull, C0, off);
+            const int pC1 = __shfl_up_sync(kFull, C1, off);
+            if (lane >= off) {
+                // new(x) = me(prev(x))
+                const int nF0 = pF0 ? F1 : F0, nC0 = pC0 + (pF0 ? C1 : C0);
+                const int nF1 = pF1 ? F1 : F0, nC1 = pC1 + (pF1 ? C1 : C0);
+                F0 = nF0; C0 = nC0; F1 = nF1; C1 = nC1;
+            }
+        }
+        // exclusive prefix for this lane given the window entry state
+        const int eF0 = __shfl_up_sync(kFull, F0, 1), eF1 = __shfl_up_sync(kFull, F1, 1);
+        const int eC0 = __shfl_up_sync(kFull, C0, 1), eC1 = __shfl_up_sync(kFull, C1, 1);
+        int st;
+        long long g;
+        if (lane == 0) {
+            st = st_coin;
+            g = coins_before;
+        } else {
+            st = st_coin ? eF1 : eF0;
+            g = coins_before + (st_coin ? eC1 : eC0);
+        }
+        // walk the slice: a coin for gene g, or the index draw of gene g-1 after a true coin
+#pragma unroll
+        for (int t = 0; t < kMutChunk; ++t) {
+            if (st) {
+                ++g;
+                st = !((tb >> t) & 1);
+            } else {
+                const long long gene = g - 1;
+                if (gene < L) {
+                    const int s = (int)(gene % I.S);
+                    const int j = (int)(gene / I.S);
+                    child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(u[t], I.M[s]);
+                }
+                st = 1;
+            }
+        }
+        const int lF0 = __shfl_sync(kFull, F0, 31), lF1 = __shfl_sync(kFull, F1, 31);
+        const int lC0 = __shfl_sync(kFull, C0, 31), lC1 = __shfl_sync(kFull, C1, 31);
+        coins_before += st_coin ? lC1 : lC0;
+        st_coin = st_coin ? lF1 : lF0;
+        pos += 32ull * kMutChunk;
+    }
+    if (lane == 0) wl.ptrs[C.item0 + cell] = child;
+}
+
+// ---------------------------------------------------------------------------- K4 pseudo breed
+// pair_step (pseudo.cpp:11-29) for one pair per warp: coin, then one mask word per 64 bits,
+// children written in place; crossed members are appended to the evaluation work list with
+// their gene rows (bits_to_int, chromosome.cpp:44-59) in the scratch arena.
+__global__ void __launch_bounds__(256) k_pseudo_breed(DevInst I, const PseudoIsland* __restrict__ isl,
+                                                       int n_islands, long long n_pairs, WorkList wl) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_pairs) return;
+    int ii = 0;
+    while (ii + 1 < n_islands && isl[ii + 1].pair0 <= warp) ++ii;
+    const PseudoIsland& P = isl[ii];
+    const int pair = (int)(warp - P.pair0);
+    const unsigned long long gen = P.st->gen;
+    const unsigned long long gen_seed = derive_seed(P.seed, gen + 1ull);  // pseudo.cpp:61
+    const unsigned long long ps = derive_seed(gen_seed, (unsigned long long)pair);  // :68
+    const bool crossed = coin_of(draw(ps, 0), P.thr_xr);
+    if (!crossed) {
+        if (lane == 0) {
+            P.mslot[2 * pair] = -1;
+            P.mslot[2 * pair + 1] = -1;
+        }
+        return;
+    }
+    unsigned long long* A = P.words + (size_t)(2 * pair) * I.words;
+    unsigned long long* B = A + I.words;
+    for (int w = lane; w < I.words; w += 32) {
+        const unsigned long long msk = draw(ps, 1ull + (unsigned long long)w);
+        const unsigned long long a = A[w], b = B[w];
+        A[w] = (a & msk) | (b & ~msk);
+        B[w] = (b & msk) | (a & ~msk);
+    }
+    long long slot = 0;
+    if (lane == 0) slot = atomicAdd(reinterpret_cast<unsigned long long*>(wl.count), 2ull);
+    slot = __shfl_sync(kFull, slot, 0);
+    __syncwarp();
+    const size_t block = (size_t)I.S * I.Jpad;
+    uint8_t* r1 = wl.scratch + (size_t)(slot - wl.scratch0) * block;
+    uint8_t* r2 = r1 + block;
+    unpack_member(I, A, r1, lane);
+    unpack_member(I, B, r2, lane);
+    if (lane == 0) {
+        wl.ptrs[slot] = r1;
+        wl.ptrs[slot + 1] = r2;
+        P.mslot[2 * pair] = slot;
+        P.mslot[2 * pair + 1] = slot + 1;
+    }
+}
+
+__global__ void k_gen_begin(long long* count, long long v) { *count = v; }
+
+// ---------------------------------------------------------------------------- K6 commit
+struct Best {
+    double f;
+    int i;
+};
+__device__ __forceinline__ Best better(Best a, Best b) {  // first index of the max
+    if (b.f > a.f || (b.f == a.f && b.i < a.i)) return b;
+    return a;
+}
+
+__device__ Best block_best(Best v) {
+    __shared__ double sf[32];
+    __shared__ int si[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        Best o{__shfl_xor_sync(kFull, v.f, off), __shfl_xor_sync(kFull, v.i, off)};
+        v = better(v, o);
+    }
+    __syncthreads();
+    if (lane == 0) { sf[wid] = v.f; si[wid] = v.i; }
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    if (wid == 0) {
+        Best x = lane < nw ? Best{sf[lane], si[lane]} : Best{-dinf(), 0x7FFFFFFF};
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            Best o{__shfl_xor_sync(kFull, x.f, off), __shfl_xor_sync(kFull, x.i, off)};
+            x = better(x, o);
+        }
+        if (lane == 0) { sf[0] = x.f; si[0] = x.i; }
+    }
+    __syncthreads();
+    return Best{sf[0], si[0]};
+}
+
+// One CTA per island.  Cellular: strict-improvement replacement into the next parity buffers
+// (cellular.cpp:153,175-180); pseudo: unconditional replacement + archive scan in pair order
+// (pseudo.cpp:74-87).  Then best_index (first max) and the per-generation trace value
+// (solver.cpp:113,121), and ++generation.
+__global__ void __launch_bounds__(1024) k_commit(DevInst I, const CellIsland* __restrict__ cells, int nc,
+                                                  const PseudoIsland* __restrict__ pseudo, int np, WorkList wl,
+                                                  int mode) {
+    // mode 0: refresh best only; 1: commit one generation; 2: pseudo init (archive over all)
+    const int advance = mode == 1;
+    const int b = blockIdx.x;
+    if (b < nc) {
+        const CellIsland& C = cells[b];
+        const int n = C.n;
+        const unsigned long long gen = C.st->gen;
+        const int q = (int)(gen & 1ull);
+        const int nq = advance ? 1 - q : q;
+        Best best{-dinf(), 0x7FFFFFFF};
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+            double f = C.fit[(size_t)q * n + c];
+            double o = C.obj[(size_t)q * n + c];
+            uint8_t s = C.sel[(size_t)q * n + c];
+            if (advance) {
+                const double cf = wl.fit[C.item0 + c];
+                if (cf > f) {
+                    f = cf;
+                    o = wl.obj[C.item0 + c];
+                    s = (uint8_t)(1 - s);
+                }
+                C.fit[(size_t)nq * n + c] = f;
+                C.obj[(size_t)nq * n + c] = o;
+                C.sel[(size_t)nq * n + c] = s;
+            }
+            best = better(best, Best{f, c});
+        }
+        best = block_best(best);
+        if (threadIdx.x == 0) {
+            IslandState* st = C.st;
+            st->best_idx = best.i;
+            st->best_fit = best.f;
+            st->best_obj = C.obj[(size_t)nq * n + best.i];
+            if (advance) {
+                C.trace[gen - st->seg_start] = st->best_obj;
+                st->gen = gen + 1ull;
+            }
+        }
+        return;
+    }
+    const PseudoIsland& P = pseudo[b - nc];
+    const int n = P.n;
+    Best live{-dinf(), 0x7FFFFFFF}, changed{-dinf(), 0x7FFFFFFF};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double f = P.fit[i];
+        if (advance) {
+            const long long k = P.mslot[i];
+            if (k >= 0) {
+                f = wl.fit[k];
+                P.fit[i] = f;
+                P.obj[i] = wl.obj[k];
+                changed = better(changed, Best{f, i});
+            }
+        } else if (mode == 2) {
+            changed = better(changed, Best{f, i});
+        }
+        live = better(live, Best{f, i});
+    }
+    live = block_best(live);
+    changed = block_best(changed);
+    IslandState* st = P.st;
+    const bool take = changed.i != 0x7FFFFFFF && changed.f > st->arch_fit;
+    if (take)
+        for (int w = threadIdx.x; w < I.words; w += blockDim.x)
+            P.archive[w] = P.words[(size_t)changed.i * I.words + w];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (take) {
+            st->arch_fit = changed.f;
+            st->arch_obj = P.obj[changed.i];
+        }
+        st->best_idx = live.i;
+        st->best_fit = live.f;
+        st->best_obj = P.obj[live.i];
+        if (advance) {
+            const unsigned long long gen = st->gen;
+            P.trace[gen - st->seg_start] = st->arch_obj;
+            st->gen = gen + 1ull;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- K5 migration
+__global__ void k_fill_seq(long long* idx, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) idx[i] = i;
+}
+
+__global__ void k_sort_keys(const double* fit, double* keys, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double f = fit[i];
+        keys[i] = (f == 0.0) ? 0.0 : f;  // canonical +0.0: radix order must match == ties
+    }
+}
+
+// cellular -> pseudo (migration.cpp:47-57): best[i] of the cellular island lands on
+// worst[N-1-i] of the pseudo island, converted with int_to_bits; the archive absorbs the
+// installs in order (pseudo.cpp:98-104).
+__global__ void k_migrate_c2p(DevInst I, CellIsland C, PseudoIsland P, const long long* best_c,
+                              const long long* worst_p, int k, int parity, const uint16_t* bit_stage) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= k) return;
+    const long long src = best_c[warp];
+    const long long dst = worst_p[P.n - 1 - warp];
+    const size_t block = (size_t)I.S * I.Jpad;
+    const uint8_t* r = C.genes + ((size_t)C.sel[(size_t)parity * C.n + src] * C.n + src) * block;
+    for (int w = lane; w < I.words; w += 32) P.words[dst * I.words + w] = pack_word(I, r, w, bit_stage);
+    if (lane == 0) {
+        P.fit[dst] = C.fit[(size_t)parity * C.n + src];
+        P.obj[dst] = C.obj[(size_t)parity * C.n + src];
+    }
+}
+
+__global__ void k_migrate_archive(DevInst I, PseudoIsland P, const long long* worst_p, int k) {
+    // consider_for_archive over the installs in order: the first strict maximum wins
+    Best b{-dinf(), 0x7FFFFFFF};
+    for (int i = threadIdx.x; i < k; i += blockDim.x) b = better(b, Best{P.fit[worst_p[P.n - 1 - i]], i});
+    b = block_best(b);
+    IslandState* st = P.st;
+    const bool take = b.i != 0x7FFFFFFF && b.f > st->arch_fit;
+    __syncthreads();
+    if (take) {
+        const long long dst = worst_p[P.n - 1 - b.i];
+        for (int w = threadIdx.x; w < I.words; w += blockDim.x) P.archive[w] = P.words[dst * I.words + w];
+        if (threadIdx.x == 0) {
+            st->arch_fit = b.f;
+            st->arch_obj = P.obj[dst];
+        }
+    }
+}
+
+// pseudo -> cellular (migration.cpp:59-69): bits_to_int into the cell's live storage slot.
+__global__ void k_migrate_p2c(DevInst I, PseudoIsland P, CellIsland C, const long long* best_p,
+                              const long long* worst_c, int k, int parity) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= k) return;
+    const long long src = best_p[warp];
+    const long long dst = worst_c[C.n - 1 - warp];
+    const size_t block = (size_t)I.S * I.Jpad;
+    uint8_t* r = C.genes + ((size_t)C.sel[(size_t)parity * C.n + dst] * C.n + dst) * block;
+    unpack_member(I, P.words + src * I.words, r, lane);
+    if (lane == 0) {
+        C.fit[(size_t)parity * C.n + dst] = P.fit[src];
+        C.obj[(size_t)parity * C.n + dst] = P.obj[src];
+    }
+}
+
+inline unsigned blocks_for(long long threads, int per_block) {
+    return (unsigned)((threads + per_block - 1) / per_block);
+}
+
+template <int G>
+int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
+    (void)sm_count;
+    cfg->G = G;
+    cfg->gl = group_layout(I.J, I.Jpad, G);
+    const int max_smem = 227 * 1024;
+    int warps = 2;
+    if ((size_t)(32 * warps / G) * cfg->gl.bytes > (size_t)max_smem) warps = 1;
+    cfg->warps = warps;
+    cfg->groups_per_cta = 32 * warps / G;
+    cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
+    if (cfg->smem > (size_t)max_smem) return -1;
+    cudaError_t e = cudaFuncSetAttribute(k_eval<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    if (e != cudaSuccess) return -2;
+    e = cudaFuncSetAttribute(k_eval<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    if (e != cudaSuccess) return -2;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval<G, false>, 32 * warps, cfg->smem);
+    if (e != cudaSuccess || occ < 1) return -2;
+    cfg->blocks_per_sm = occ;
+    return 0;
+}
+
+template <int G>
+cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,
+                          int sm_count, bool schedule, cudaStream_t st) {
+    long long blocks = (max_items + cfg.groups_per_cta - 1) / cfg.groups_per_cta;
+    const long long cap = (long long)cfg.blocks_per_sm * sm_count;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (schedule)
+        k_eval<G, true><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+    else
+        k_eval<G, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int eval_config(const DevInst& I, int sm_count, EvalConfig* cfg) {
+    if (I.maxM <= 4) return eval_config_g<4>(I, sm_count, cfg);
+    if (I.maxM <= 8) return eval_config_g<8>(I, sm_count, cfg);
+    if (I.maxM <= 16) return eval_config_g<16>(I, sm_count, cfg);
+    if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, cfg);
+    return -3;
+}
+
+cudaError_t launch_eval(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,
+                        int sm_count, bool schedule, cudaStream_t st) {
+    switch (cfg.G) {
+        case 4: return launch_eval_g<4>(I, cfg, W, max_items, sm_count, schedule, st);
+        case 8: return launch_eval_g<8>(I, cfg, W, max_items, sm_count, schedule, st);
+        case 16: return launch_eval_g<16>(I, cfg, W, max_items, sm_count, schedule, st);
+        case 32: return launch_eval_g<32>(I, cfg, W, max_items, sm_count, schedule, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_random_rows(const DevInst& I, uint8_t* out, long long stride, long long n,
+                               unsigned long long base, long long first, bool per_item, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_random_rows<<<blocks_for(n * 32, 256), 256, 0, st>>>(I, out, stride, n, base, first, per_item ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_bits(const DevInst& I, const uint8_t* rows, long long row_stride, const long long* src_idx,
+                             unsigned long long* words, const long long* dst_idx, long long n, bool with_complement,
+                             const uint16_t* bit_stage, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_pack_bits<<<blocks_for(n * 32, 256), 256, 0, st>>>(I, rows, row_stride, src_idx, words, dst_idx, n,
+                                                        with_complement ? 1 : 0, bit_stage);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_rows(const DevInst& I, const unsigned long long* words, const long long* src_idx,
+                               uint8_t* rows, long long row_stride, const long long* dst_idx, long long n,
+                               cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_unpack_rows<<<blocks_for(n * 32, 256), 256, 0, st>>>(I, words, src_idx, rows, row_stride, dst_idx, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_from_int(const DevInst& I, const int32_t* gi, const uint8_t* gu, uint8_t* rows, long long n,
+                                 cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_rows_from_int<<<blocks_for(n * 32, 256), 256, 0, st>>>(I, gi, gu, rows, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_to_int(const DevInst& I, const uint8_t* rows, long long row_stride, const long long* src_idx,
+                               int32_t* out, long long n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_rows_to_int<<<blocks_for(n * 32, 256), 256, 0, st>>>(I, rows, row_stride, src_idx, out, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_breed(const DevInst& I, const CellIsland* cells_dev, int nc, long long n_cells,
+                         const PseudoIsland* pseudo_dev, int np, long long n_pairs, const WorkList& wl,
+                         cudaStream_t st) {
+    k_gen_begin<<<1, 1, 0, st>>>(wl.count, n_cells);
+    if (n_cells > 0) k_cell_breed<<<blocks_for(n_cells * 32, 256), 256, 0, st>>>(I, cells_dev, nc, n_cells, wl);
+    if (n_pairs > 0) k_pseudo_breed<<<blocks_for(n_pairs * 32, 256), 256, 0, st>>>(I, pseudo_dev, np, n_pairs, wl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_commit(const DevInst& I, const CellIsland* cells_dev, int nc, const PseudoIsland* pseudo_dev,
+                          int np, const WorkList& wl, cudaStream_t st) {
+    k_commit<<<nc + np, 1024, 0, st>>>(I, cells_dev, nc, pseudo_dev, np, wl, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_island_stats(const DevInst& I, const CellIsland* cells_dev, int nc, const PseudoIsland* pseudo_dev,
+                                int np, int mode, cudaStream_t st) {
+    if (nc + np == 0) return cudaSuccess;
+    WorkList wl{};
+    k_commit<<<nc + np, 1024, 0, st>>>(I, cells_dev, nc, pseudo_dev, np, wl, mode);
+    return cudaGetLastError();
+}
+
+size_t sort_temp_bytes(long long n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const double*)nullptr, (double*)nullptr,
+                                              (const long long*)nullptr, (long long*)nullptr, (int)n);
+    return bytes;
+}
+
+cudaError_t launch_sort_desc(const double* fit, long long n, double* keys_tmp, double* keys_out, long long* idx_in,
+                             long long* idx_out, void* temp, size_t temp_bytes, cudaStream_t st) {
+    k_sort_keys<<<blocks_for(n, 256), 256, 0, st>>>(fit, keys_tmp, n);
+    k_fill_seq<<<blocks_for(n, 256), 256, 0, st>>>(idx_in, n);
+    // stable radix sort: fitness descending, equal keys keep ascending index (sort_island,
+    // cellular.cpp:29-36)
+    return cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, keys_tmp, keys_out, idx_in, idx_out, (int)n,
+                                                     0, 64, st);
+}
+
+cudaError_t launch_migrate_c2p(const DevInst& I, const CellIsland& c, const PseudoIsland& p, const long long* best_c,
+                               const long long* worst_p, int k, int parity, const uint16_t* bit_stage,
+                               cudaStream_t st) {
+    if (k <= 0) return cudaSuccess;
+    k_migrate_c2p<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, c, p, best_c, worst_p, k, parity, bit_stage);
+    k_migrate_archive<<<1, 1024, 0, st>>>(I, p, worst_p, k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_migrate_p2c(const DevInst& I, const PseudoIsland& p, const CellIsland& c, const long long* best_p,
+                               const long long* worst_c, int k, int parity, cudaStream_t st) {
+    if (k <= 0) return cudaSuccess;
+    k_migrate_p2c<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, p, c, best_p, worst_c, k, parity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_seq(long long* idx, long long n, cudaStream_t st) {
+    k_fill_seq<<<blocks_for(n, 256), 256, 0, st>>>(idx, n);
+    return cudaGetLastError();
+}
+
+}  // namespace ffsga_dev

@@ -1,0 +1,133 @@
+"""K1/K7 parity: the CUDA decoder against the C restatement and the compiled reference, bitwise."""
+import numpy as np
+import pytest
+
+from conftest import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi():
+    from paper_1903_10722_b200 import capi
+    assert capi.device_count() > 0, "no GPU: the device path has no CPU fallback"
+    return capi
+
+
+def micro(orc):
+    from pyoracle import InstanceData
+    # test_model.cpp:18-31: J=2, S=2, M=[2,1]
+    return InstanceData(2, 2, [2, 1], [2, 3, 4, 2, 3, 1], [0, 0], [10, 10], 100.0)
+
+
+def test_micro_schedule(capi, orc):
+    d = micro(orc)
+    inst = capi.Instance.from_data(d, 211.0)
+    m, s, c, rep = inst.decode([0, 0, 0, 0])
+    # test_model.cpp:57-69
+    assert (s[0], c[0]) == (0.0, 2.0)
+    assert (s[2], c[2]) == (2.0, 4.0)
+    assert (s[1], c[1]) == (2.0, 6.0)
+    assert (s[3], c[3]) == (6.0, 7.0)
+    # test_model.cpp:79-88
+    assert rep == dict(makespan=7.0, total_tardiness=0.0, objective=7.0, fitness=204.0, emax_used=211.0)
+    obj, fit = capi.Instance.from_data(d, 5.0).evaluate([[0, 0, 0, 0]])
+    assert obj[0] == 7.0 and fit[0] == 0.0  # test_model.cpp:90-95
+
+
+def test_bad_gene_messages(capi, orc):
+    d = micro(orc)
+    inst = capi.Instance.from_data(d, 211.0)
+    with pytest.raises(ValueError, match="out of range"):
+        inst.evaluate([[0, 1, 0, 0]])
+    with pytest.raises(ValueError, match="out of range"):
+        inst.evaluate([[-1, 0, 0, 0]])
+    # message matches the reference's first offending gene in dispatch order
+    oi = orc.instance(d)
+    for genes in ([0, 1, 0, 0], [-1, 0, 0, 0], [0, 0, 5, 0], [0, 7, 0, 7]):
+        with pytest.raises(ValueError) as a:
+            inst.evaluate([genes])
+        with pytest.raises(ValueError) as b:
+            oi.score(genes, 211.0)
+        assert str(a.value).split(" (")[0] == str(b.value)
+
+
+SHAPES = [(20, 5, 3, 3), (6, 2, 2, 2), (100, 10, 2, 5), (100, 20, 2, 8), (500, 20, 2, 8), (37, 7, 1, 8),
+          (64, 3, 5, 16), (30, 4, 9, 32), (1, 2, 1, 2), (3, 2, 2, 2)]
+
+
+@pytest.mark.parametrize("J,S,lo,hi", SHAPES)
+def test_random_batch_bitwise(capi, orc, J, S, lo, hi):
+    d = synthetic(orc, J, S, lo, hi)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    n = 300 if J * S <= 2000 else 60
+    pop = oi.random_population(99, 0, n)
+    obj, fit, mk, td = inst.evaluate(pop, full=True)
+    eo, ef, em, et = oi.score_batch(pop, emax)
+    for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_integer_times_ties(capi, orc):
+    # integer processing times make equal completions (ties broken by job index) common
+    for seed in range(5):
+        d = orc.generate(40, 6, [2, 3, 4, 2, 3, 2], weight=1.0, seed=seed, integer_times=True)
+        oi = orc.instance(d)
+        emax = oi.estimate_emax()
+        pop = oi.random_population(seed, 0, 400)
+        obj, fit = capi.Instance.from_data(d, emax).evaluate(pop)
+        eo, ef, _, _ = oi.score_batch(pop, emax)
+        assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
+
+
+def test_decode_schedule_matches_reference(capi, orc):
+    d = synthetic(orc, 50, 6)
+    oi = orc.instance(d)
+    inst = capi.Instance.from_data(d, oi.estimate_emax())
+    for g in oi.random_population(5, 0, 10):
+        m, s, c, rep = inst.decode(g)
+        e = oi.score(g, oi.estimate_emax(), schedule=True)
+        assert np.array_equal(m, e["machine"]) and np.array_equal(s, e["start"])
+        assert np.array_equal(c, e["completion"]) and rep["objective"] == e["objective"]
+
+
+def test_device_random_population_matches(capi, orc):
+    d = synthetic(orc, 100, 10, 2, 5)
+    oi = orc.instance(d)
+    inst = capi.Instance.from_data(d, oi.estimate_emax())
+    b = capi.Batch(inst, 1000)
+    b.fill_random(99, 12345, 1000)
+    got = b.download(0, 1000)
+    want = oi.random_population(99, 12345, 1000)
+    assert np.array_equal(got, want)
+    b.evaluate(1000)
+    obj, fit = b.results(1000)
+    eo, ef, _, _ = oi.score_batch(want, oi.estimate_emax())
+    assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
+
+
+def test_exhaustive_small_instances(capi, orc):
+    # acceptance criterion 2 (acceptance_main.cpp:161-215): J=3..5, S=2, M=2, all assignments
+    import itertools
+    for seed in range(6):
+        J = 3 + seed % 3
+        d = orc.generate(J, 2, [2, 2], seed=100 + seed)
+        oi = orc.instance(d)
+        emax = oi.estimate_emax()
+        pop = np.array(list(itertools.product([0, 1], repeat=2 * J)), dtype=np.int32)
+        obj, _ = capi.Instance.from_data(d, emax).evaluate(pop)
+        sel = np.array([oi.simulate_selection(g)["objective"] for g in pop])
+        assert np.array_equal(obj, sel)
+
+
+def test_against_compiled_reference(capi, orc, ref):
+    d = synthetic(orc, 500, 20)
+    ri = ref.instance(d)
+    emax = ri.estimate_emax()
+    pop = ri.random_population(99, 0, 200)
+    obj, fit, mk, td = capi.Instance.from_data(d, emax).evaluate(pop, full=True)
+    eo, ef, em, et = ri.score_batch(pop, emax, workers=8)
+    assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
+    assert np.array_equal(mk, em) and np.array_equal(td, et)
