@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""Benchmark of the FFS hot path on B200: GA generations/s and makespan evaluations/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ga|decoder]
+
+Workload (default "ga", BASELINE.json configs[2] = SURVEY 8(d) C3): synthetic 500 jobs x 20 stages,
+machines per stage in [2, 8] (M[s] = 2 + Rng(1000 + J*S).next_index(7)), generator seed 7,
+weight 100; 8 islands = 4 couples of (cellular 128x64, pseudo 8192), total population 65536,
+gap 500, theta 1, seed 1.  One step = one GA generation of every island (all selection,
+crossover, mutation, decode/evaluate, replacement, archive and trace work).  Under torchrun the
+8 islands are sharded over the ranks (couples kept together while ranks <= 4): total work is
+fixed, so scaling is "strong"; value = generations/s of the whole job (the same generation on
+every island, device time max over ranks).
+
+"decoder" workload: 1M random chromosomes of the 500x20 instance evaluated per
+launch; one step = one launch.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, the unmodified
+reference sources compiled by oracle/Makefile) on this box's host cores with all of them as
+workers, same config and metric.  Under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FFS makespan evals/sec & GA generations/sec at 1/2/4/8 B200 vs CPU ref"
+J, S, LO, HI, GEN_SEED, WEIGHT = 500, 20, 2, 8, 7, 100.0
+COUPLES, ISLAND_POP, GRID = 4, 8192, (128, 64)
+RUN_SEED, GAP, THETA = 1, 500, 1.0
+SWEEP_N = 1 << 20
+
+
+def synthetic_machines(jobs, stages, lo=LO, hi=HI):
+    from paper_1903_10722_b200.islands import splitmix_next
+    st = 1000 + jobs * stages
+    out = []
+    for _ in range(stages):
+        st, u = splitmix_next(st)
+        unit = float(u >> 11) * 2.0 ** -53
+        v = int(unit * float(hi - lo + 1))
+        out.append(lo + min(v, hi - lo))
+    return out
+
+
+def make_instance():
+    """Synthetic C3 instance through the product's host generator."""
+    from paper_1903_10722_b200 import generate_instance, estimate_emax
+    inst = generate_instance(jobs=J, stages=S, machines=synthetic_machines(J, S), weight=WEIGHT, seed=GEN_SEED)
+    return inst, estimate_emax(inst)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_baseline_ga(inst_data, emax, workers):
+    """Reference CPU generation on a bounded sample: one couple (CellGrid 128x64 + PairPopulation
+    8192) of the 4, one generation each, workers = host threads; scaled to the 8-island step."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import RefLib, have_ref
+    if not have_ref():
+        return None
+    from paper_1903_10722_b200.islands import derive_seed
+    ref = RefLib()
+    ri = ref.instance(inst_data)
+    c = ri.cellular(emax, ISLAND_POP, derive_seed(RUN_SEED, 0), width=GRID[0], height=GRID[1])
+    p = ri.pseudo(emax, ISLAND_POP, derive_seed(RUN_SEED, 1))
+    c.step(workers)
+    p.step(workers)
+    t0 = time.perf_counter()
+    reps = 2
+    for _ in range(reps):
+        c.step(workers)
+        p.step(workers)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": 1.0 / (COUPLES * dt), "unit": "generations/s", "cores": workers, "kind": "reference",
+            "sample": f"{reps} generations of 1 of {COUPLES} couples (CellGrid 128x64 + PairPopulation 8192, "
+                      f"oracle/_ref, workers={workers}), time x{COUPLES}"}
+
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import RefLib, have_ref
+    if not have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libffsga_ref.so not built"}))
+        return 0
+    from pyoracle import InstanceData
+    from paper_1903_10722_b200.islands import derive_seed
+    workers = os.cpu_count() or 1
+    ref = RefLib()
+    m = synthetic_machines(J, S)
+    data = ref.generate(J, S, m, weight=WEIGHT, seed=GEN_SEED)
+    ri = ref.instance(data)
+    emax = ri.estimate_emax()
+    if args.workload == "decoder":
+        n = 20000
+        pop = ri.random_population(99, 0, n)
+        for _ in range(args.warmup):
+            ri.score_batch(pop[:2000], emax, workers)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ri.score_batch(pop, emax, workers)
+        dt = time.perf_counter() - t0
+        val = n * args.steps / dt
+        unit = "evals/s"
+        sample = f"{n} chromosomes per step (of the 1M launch), Evaluator::score via parallel_chunks"
+        cfg = {"workload": "C5 decoder sweep 500x20, M in [2,8]", "n_per_step_sampled": n}
+    else:
+        isl = []
+        for i in range(2 * COUPLES):
+            if i % 2 == 0:
+                isl.append(ri.cellular(emax, ISLAND_POP, derive_seed(RUN_SEED, i), width=GRID[0], height=GRID[1]))
+            else:
+                isl.append(ri.pseudo(emax, ISLAND_POP, derive_seed(RUN_SEED, i)))
+        for _ in range(args.warmup):
+            for x in isl:
+                x.step(workers)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for x in isl:
+                x.step(workers)
+        dt = time.perf_counter() - t0
+        val = args.steps / dt
+        unit = "generations/s"
+        sample = (f"full C3 generation per step: 4 CellGrid 128x64 + 4 PairPopulation 8192 steps, "
+                  f"workers={workers}")
+        cfg = ga_config(world)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": unit, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": val, "unit": unit, "cores": workers, "kind": "reference", "sample": sample},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+    return 0
+
+
+def ga_config(world):
+    return {"workload": "C3: FFS 500 jobs x 20 stages x 2-8 machines/stage, 8 islands (4 cellular 128x64 + "
+                        "4 pseudo 8192), pop 65536",
+            "jobs": J, "stages": S, "machines": synthetic_machines(J, S), "islands": 2 * COUPLES,
+            "population": 2 * COUPLES * ISLAND_POP, "gap": GAP, "theta": THETA, "seed": RUN_SEED,
+            "ranks": world, "islands_per_rank": 2 * COUPLES // world if world <= 2 * COUPLES else None,
+            "l2": "inputs larger than L2 (resident population 0.77 GB > 126 MB)"}
+
+
+def decoder_sweep(inst_data, emax, device, steps, warmup):
+    """C5: 1M random chromosomes per launch (K2 fill, then K1 launches timed with events)."""
+    from paper_1903_10722_b200 import capi
+    ci = capi.Instance.from_data(inst_data, emax, device)
+    b = capi.Batch(ci, SWEEP_N)
+    b.fill_random(99, 0, SWEEP_N)
+    for _ in range(max(1, warmup)):
+        b.evaluate(SWEEP_N)
+    b.sync()
+    ms = []
+    for _ in range(max(1, steps)):
+        b.evaluate(SWEEP_N)
+        ms.append(b.last_eval_ms())
+    avg = float(np.mean(ms))
+    L = J * S
+    bytes_per = SWEEP_N * (L + 16)
+    obj, _ = b.results(SWEEP_N)
+    return {"evals_per_s": SWEEP_N / (avg / 1e3), "n_per_launch": SWEEP_N, "ms_per_launch": avg,
+            "dispatches_per_s": SWEEP_N * L / (avg / 1e3),
+            "roofline": {"bound": "hbm", "achieved": bytes_per / (avg / 1e3) / 1e9, "unit": "GB/s",
+                         "traffic": None, "algorithmic_bytes_per_launch": bytes_per},
+            "checksum_objective_sum": float(np.sum(obj))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="ga", choices=["ga", "decoder"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1903_10722_b200.islands import TorchComm
+        comm = TorchComm(device=f"cuda:{local}")
+
+    from paper_1903_10722_b200 import capi
+    from paper_1903_10722_b200.islands import IslandConfig, IslandModel
+    inst, emax = make_instance()
+    from paper_1903_10722_b200 import instance_arrays
+    data = instance_arrays(inst)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    def barrier():
+        if comm is not None:
+            comm.barrier()
+
+    cfg = IslandConfig(couples=COUPLES, island_population=ISLAND_POP, generations=args.steps, migration_gap=GAP,
+                       theta=THETA, seed=RUN_SEED, grid_shape=GRID)
+    model = IslandModel(data, emax, cfg, comm, device=local)
+    L = J * S
+    if args.workload == "ga":
+        model.advance(args.warmup)
+        model.inst.set_timing(True)
+        model.inst.reset_timing()
+        ev0 = model.inst.evaluations()
+        torch.cuda.synchronize()
+        barrier()
+        l0 = capi.launch_count()
+        with ClockSampler(local) as clk:
+            model.advance(args.steps)
+            dev_ms = model.inst.last_step_ms()
+        l1 = capi.launch_count()
+        evals = model.inst.evaluations() - ev0
+        eval_ms, eval_n = model.inst.timing(0)
+        breed_ms, _ = model.inst.timing(1)
+        commit_ms, _ = model.inst.timing(2)
+        model.inst.set_timing(False)
+        barrier()
+        if comm is not None:
+            agg = comm.allgather(np.array([dev_ms, evals, eval_ms, eval_n], dtype=np.float64))
+            ms_max = float(agg[:, 0].max())
+            evals_all = float(agg[:, 1].sum())
+        else:
+            ms_max, evals_all = dev_ms, float(evals)
+        gens_per_s = args.steps / (ms_max / 1e3)
+        algo_bytes = evals * (L + 16)
+        achieved = algo_bytes / (eval_ms / 1e3) / 1e9 if eval_ms > 0 else 0.0
+
+        # e2e: the public API call a user makes (instance upload, island init, K generations,
+        # traces + champion back to the host), wall clock
+        barrier()
+        t0 = time.perf_counter()
+        inst2, emax2 = make_instance()
+        cfg2 = IslandConfig(couples=COUPLES, island_population=ISLAND_POP, generations=args.steps,
+                            migration_gap=GAP, theta=THETA, seed=RUN_SEED, grid_shape=GRID)
+        model2 = IslandModel(instance_arrays(inst2), emax2, cfg2, comm, device=local)
+        res = model2.run()
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if comm is not None:
+            e2e_s = float(comm.allgather(np.array([e2e_s]))[:, 0].max())
+        h2d = (L * sum(synthetic_machines(J, S)) + 2 * J) * 8 + S * 4
+        d2h = 2 * COUPLES * args.steps * 8 + L * 4 + 5 * 8
+        del model2
+
+        sweep = None
+        if world == 1 and not args.no_sweep:
+            sweep = decoder_sweep(data, emax, local, 3, 1)
+            sweep["roofline"]["peak"] = hbm_peak
+            sweep["roofline"]["frac"] = sweep["roofline"]["achieved"] / hbm_peak
+        cpu = None
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_ga(data, emax, os.cpu_count() or 1)
+        if rank == 0:
+            line = {
+                "metric": METRIC, "value": gens_per_s, "unit": "generations/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SURVEY 8(d) generator convention, random-init populations)",
+                "config": ga_config(world),
+                "evals_per_s": evals_all / (ms_max / 1e3),
+                "evals_per_step": evals_all / args.steps,
+                "kernel_ms_per_step": {"eval": eval_ms / args.steps, "breed": breed_ms / args.steps,
+                                       "commit": commit_ms / args.steps},
+                "roofline": {"bound": "hbm", "kernel": "k_eval (K1 decoder)", "achieved": achieved,
+                             "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                             "frac": achieved / hbm_peak, "traffic": None,
+                             "algorithmic_bytes_per_eval": L + 16,
+                             "note": "decoder is latency/issue bound (fp64 max/add chains + smem list "
+                                     "merges); see profiles/ for issue-active and DRAM counters"},
+                "e2e": {"value": args.steps / e2e_s, "unit": "generations/s",
+                        "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                        "what": "generate instance + IslandModel init + run(K generations) + traces/champion D2H",
+                        "best_objective": res.best_report["objective"]},
+                "gpu_launches": int(l1 - l0),
+                "clocks": clk.summary(),
+                "cpu_baseline": cpu,
+                "decoder_sweep": sweep,
+            }
+            print(json.dumps(line), flush=True)
+    else:  # decoder workload
+        ci = model.inst
+        b = capi.Batch(ci, SWEEP_N)
+        b.fill_random(99, 0, SWEEP_N)
+        for _ in range(args.warmup):
+            b.evaluate(SWEEP_N)
+        b.sync()
+        barrier()
+        l0 = capi.launch_count()
+        ms = []
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                b.evaluate(SWEEP_N)
+                ms.append(b.last_eval_ms())
+        l1 = capi.launch_count()
+        tot = float(np.sum(ms))
+        if comm is not None:
+            tot = float(comm.allgather(np.array([tot]))[:, 0].max())
+        val = world * SWEEP_N * args.steps / (tot / 1e3)
+        # e2e: host u8 genes -> device -> evaluate -> results back, through the C ABI
+        host = b.download(0, 4096).astype(np.uint8)
+        n_e2e = 65536
+        hostbig = np.ascontiguousarray(np.tile(host, (n_e2e // 4096, 1)))
+        t0 = time.perf_counter()
+        for _ in range(2):
+            ci.evaluate(hostbig)
+        e2e = 2 * n_e2e / (time.perf_counter() - t0)
+        if rank == 0:
+            achieved = SWEEP_N * (L + 16) / (tot / args.steps / 1e3) / 1e9
+            print(json.dumps({
+                "metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C5 decoder sweep: 1M random chromosomes per launch, 500x20, M in [2,8]",
+                           "l2": "inputs larger than L2 (10.7 GB of genes per launch)"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": achieved / hbm_peak, "traffic": None},
+                "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": n_e2e * L,
+                        "d2h_bytes_per_step": n_e2e * 16},
+                "gpu_launches": int(l1 - l0), "clocks": clk.summary()}), flush=True)
+    if comm is not None:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -82,7 +82,7 @@ def build_host(force=False):
     lib = os.path.join(PKG, "libffsga.so")
     cuda_lib = os.path.join(PKG, "libffsga_cuda.so")
     if force or _newer(lib, srcs + hdrs + [cuda_lib]):
-        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra"] + inc + srcs +
+        _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-dangling-reference"] + inc + srcs +
              ["-L" + PKG, "-lffsga_cuda", "-Wl,-rpath,$ORIGIN", "-o", lib])
     import pybind11
     mod_src = os.path.join(CSRC, "bindings", "module.cpp")
@@ -90,7 +90,7 @@ def build_host(force=False):
         return lib
     mod = os.path.join(PKG, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
     if force or _newer(mod, [mod_src, lib] + hdrs):
-        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared"] + inc +
+        _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared"] + inc +
              ["-I" + pybind11.get_include(), "-I" + sysconfig.get_paths()["include"], mod_src,
               "-L" + PKG, "-lffsga", "-lffsga_cuda", "-Wl,-rpath,$ORIGIN", "-o", mod])
     return lib

@@ -125,6 +125,12 @@ int ffsga_cuda_cellular_genes(ffsga_cuda_cellular c, int index, int32_t* genes);
 int ffsga_cuda_cellular_slots(ffsga_cuda_cellular c, int index, int32_t* slots);
 /* best_index / best_fitness / best_objective (cellular.cpp:184-189) */
 int ffsga_cuda_cellular_best(ffsga_cuda_cellular c, int* index, double* fitness, double* objective);
+/* cell_candidate (cellular.cpp:157-162): compute_cell of `index` against the current state on
+ * the stream whose state is `stream_state` (the state of an ffsga::Rng).  Returns the candidate
+ * (child if replaced, else the current cell) and how many draws the reference consumes, so the
+ * caller can advance its Rng. */
+int ffsga_cuda_cellular_candidate(ffsga_cuda_cellular c, int index, uint64_t stream_state, int32_t* genes,
+                                  double* fitness, double* objective, int* replaced, uint64_t* draws_used);
 /* install (cellular.cpp:191-195) */
 int ffsga_cuda_cellular_install(ffsga_cuda_cellular c, int index, const int32_t* genes, double fitness,
                                 double objective);
@@ -142,6 +148,8 @@ int ffsga_cuda_pseudo_member(ffsga_cuda_pseudo p, int index, uint8_t* bits);
 int ffsga_cuda_pseudo_best(ffsga_cuda_pseudo p, int* index, double* fitness, double* objective);
 /* archive_chromosome / archive_fitness / archive_objective (pseudo.hpp:58-60); bits may be NULL */
 int ffsga_cuda_pseudo_archive(ffsga_cuda_pseudo p, double* fitness, double* objective, uint8_t* bits);
+/* bits_to_int(archive_chromosome()) as job-major int32 genes (solver.cpp:182) */
+int ffsga_cuda_pseudo_archive_genes(ffsga_cuda_pseudo p, int32_t* genes);
 /* install (pseudo.cpp:98-104): the archive absorbs the installed score */
 int ffsga_cuda_pseudo_install(ffsga_cuda_pseudo p, int index, const uint8_t* bits, double fitness,
                               double objective);
@@ -163,6 +171,18 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int n_cells, const ffsga_c
 int ffsga_cuda_migrate_cellular_to_pseudo(ffsga_cuda_cellular from, ffsga_cuda_pseudo to, int k);
 int ffsga_cuda_migrate_pseudo_to_cellular(ffsga_cuda_pseudo from, ffsga_cuda_cellular to, int k);
 
+/* Cross-device migration halves (the same transfer as above, split at the wire so the rows can
+ * travel between GPUs): export the k best of one island in sort_island order, import them over
+ * the k worst of the other (best lands on worst).  Cellular islands export job-major int32
+ * genes and import bit chromosomes (bits_to_int on the device); pseudo islands export bit
+ * chromosomes (one byte per bit) and import int32 genes (int_to_bits on the device). */
+int ffsga_cuda_cellular_export(ffsga_cuda_cellular c, int k, int32_t* genes, double* fitness, double* objective);
+int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* fitness, double* objective);
+int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits, const double* fitness,
+                               const double* objective);
+int ffsga_cuda_pseudo_import(ffsga_cuda_pseudo p, int k, const int32_t* genes, const double* fitness,
+                             const double* objective);
+
 /* ---- measurement ------------------------------------------------------------------------------
  * Per-kernel CUDA-event timing on the launching stream (off by default).  When enabled, every
  * k_eval launch of a batch or of ffsga_cuda_step is bracketed by events; totals accumulate. */
@@ -170,6 +190,11 @@ int ffsga_cuda_set_timing(ffsga_cuda_instance inst, int enabled);
 /* total milliseconds and launch count of: 0 = K1 eval, 1 = K3+K4 breed, 2 = K6 commit */
 int ffsga_cuda_timing(ffsga_cuda_instance inst, int which, double* ms, int64_t* launches);
 int ffsga_cuda_reset_timing(ffsga_cuda_instance inst);
+/* makespan evaluations performed by ffsga_cuda_step on this instance since creation
+ * (cellular children + crossed pseudo members; device counter) */
+int ffsga_cuda_evaluations(ffsga_cuda_instance inst, int64_t* count);
+/* device milliseconds of the last ffsga_cuda_step launch sequence (events on its stream) */
+int ffsga_cuda_last_step_ms(ffsga_cuda_instance inst, float* ms);
 /* kernels launched by this library since load (all kinds) */
 int ffsga_cuda_launch_count(int64_t* count);
 

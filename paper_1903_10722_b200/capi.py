@@ -71,6 +71,7 @@ _SIGS = {
     "ffsga_cuda_cellular_slots": (_i32, [_vp, _i32, _pi32]),
     "ffsga_cuda_cellular_best": (_i32, [_vp, C.POINTER(_i32), _pd, _pd]),
     "ffsga_cuda_cellular_install": (_i32, [_vp, _i32, _pi32, _f64, _f64]),
+    "ffsga_cuda_cellular_candidate": (_i32, [_vp, _i32, _u64, _pi32, _pd, _pd, C.POINTER(_i32), C.POINTER(_u64)]),
     "ffsga_cuda_pseudo_create": (_i32, [_vp, _i32, _f64, _u64, _pvp]),
     "ffsga_cuda_pseudo_destroy": (_i32, [_vp]),
     "ffsga_cuda_pseudo_size": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
@@ -80,9 +81,16 @@ _SIGS = {
     "ffsga_cuda_pseudo_best": (_i32, [_vp, C.POINTER(_i32), _pd, _pd]),
     "ffsga_cuda_pseudo_archive": (_i32, [_vp, _pd, _pd, _pu8]),
     "ffsga_cuda_pseudo_install": (_i32, [_vp, _i32, _pu8, _f64, _f64]),
+    "ffsga_cuda_pseudo_archive_genes": (_i32, [_vp, _pi32]),
     "ffsga_cuda_step": (_i32, [_pvp, _i32, _pvp, _i32, _i32, _pd, _pd]),
     "ffsga_cuda_migrate_cellular_to_pseudo": (_i32, [_vp, _vp, _i32]),
     "ffsga_cuda_migrate_pseudo_to_cellular": (_i32, [_vp, _vp, _i32]),
+    "ffsga_cuda_cellular_export": (_i32, [_vp, _i32, _pi32, _pd, _pd]),
+    "ffsga_cuda_pseudo_export": (_i32, [_vp, _i32, _pu8, _pd, _pd]),
+    "ffsga_cuda_cellular_import": (_i32, [_vp, _i32, _pu8, _pd, _pd]),
+    "ffsga_cuda_pseudo_import": (_i32, [_vp, _i32, _pi32, _pd, _pd]),
+    "ffsga_cuda_last_step_ms": (_i32, [_vp, C.POINTER(C.c_float)]),
+    "ffsga_cuda_evaluations": (_i32, [_vp, C.POINTER(_i64)]),
     "ffsga_cuda_set_timing": (_i32, [_vp, _i32]),
     "ffsga_cuda_timing": (_i32, [_vp, _i32, _pd, C.POINTER(_i64)]),
     "ffsga_cuda_reset_timing": (_i32, [_vp]),
@@ -202,6 +210,16 @@ class Instance:
         _check(lib().ffsga_cuda_decode(self.h, _p(g, _pi32), _p(m, _pi32), _p(s, _pd), _p(c, _pd), _p(r, _pd)))
         rep = dict(makespan=r[0], total_tardiness=r[1], objective=r[2], fitness=r[3], emax_used=r[4])
         return m, s, c, rep
+
+    def last_step_ms(self):
+        ms = C.c_float()
+        _check(lib().ffsga_cuda_last_step_ms(self.h, C.byref(ms)))
+        return ms.value
+
+    def evaluations(self):
+        n = C.c_int64()
+        _check(lib().ffsga_cuda_evaluations(self.h, C.byref(n)))
+        return n.value
 
     def set_timing(self, on=True):
         _check(lib().ffsga_cuda_set_timing(self.h, int(on)))
@@ -328,6 +346,28 @@ class Cellular:
         g = np.ascontiguousarray(genes, dtype=np.int32)
         _check(lib().ffsga_cuda_cellular_install(self.h, index, _p(g, _pi32), fit, obj))
 
+    def candidate(self, index, stream_state):
+        """compute_cell on an explicit stream -> (genes, fitness, objective, replaced, draws_used)."""
+        g = np.empty(self.inst.num_genes, dtype=np.int32)
+        f, o, r, d = C.c_double(), C.c_double(), C.c_int(), C.c_uint64()
+        _check(lib().ffsga_cuda_cellular_candidate(self.h, index, stream_state, _p(g, _pi32), C.byref(f), C.byref(o),
+                                                   C.byref(r), C.byref(d)))
+        return g, f.value, o.value, bool(r.value), d.value
+
+    def export_best(self, k):
+        """k best cells in sort_island order -> (genes [k, L] int32, fitness, objective)."""
+        g = np.empty((k, self.inst.num_genes), dtype=np.int32)
+        f, o = np.empty(k), np.empty(k)
+        _check(lib().ffsga_cuda_cellular_export(self.h, k, _p(g, _pi32), _p(f, _pd), _p(o, _pd)))
+        return g, f, o
+
+    def import_worst(self, bits, fit, obj):
+        """Install k pseudo migrants (bit chromosomes) over the k worst cells."""
+        b = np.ascontiguousarray(bits, dtype=np.uint8)
+        f = np.ascontiguousarray(fit, dtype=np.float64)
+        o = np.ascontiguousarray(obj, dtype=np.float64)
+        _check(lib().ffsga_cuda_cellular_import(self.h, len(f), _p(b, _pu8), _p(f, _pd), _p(o, _pd)))
+
 
 class Pseudo:
     """Device complementary-pair island (ffsga_cuda_pseudo ~ PairPopulation)."""
@@ -381,9 +421,29 @@ class Pseudo:
         _check(lib().ffsga_cuda_pseudo_archive(self.h, C.byref(f), C.byref(o), _p(bits, _pu8)))
         return bits[: self.total_bits], f.value, o.value
 
+    def archive_genes(self):
+        """bits_to_int(archive_chromosome()) computed on the device."""
+        out = np.empty(self.inst.num_genes, dtype=np.int32)
+        _check(lib().ffsga_cuda_pseudo_archive_genes(self.h, _p(out, _pi32)))
+        return out
+
     def install(self, index, bits, fit, obj):
         b = np.ascontiguousarray(bits, dtype=np.uint8)
         _check(lib().ffsga_cuda_pseudo_install(self.h, index, _p(b, _pu8), fit, obj))
+
+    def export_best(self, k):
+        """k best members in sort_island order -> (bits [k, total_bits] uint8, fitness, objective)."""
+        b = np.empty((k, max(self.total_bits, 1)), dtype=np.uint8)
+        f, o = np.empty(k), np.empty(k)
+        _check(lib().ffsga_cuda_pseudo_export(self.h, k, _p(b, _pu8), _p(f, _pd), _p(o, _pd)))
+        return b[:, : self.total_bits], f, o
+
+    def import_worst(self, genes, fit, obj):
+        """Install k cellular migrants (int genes) over the k worst members; archive absorbs them."""
+        g = np.ascontiguousarray(genes, dtype=np.int32)
+        f = np.ascontiguousarray(fit, dtype=np.float64)
+        o = np.ascontiguousarray(obj, dtype=np.float64)
+        _check(lib().ffsga_cuda_pseudo_import(self.h, len(f), _p(g, _pi32), _p(f, _pd), _p(o, _pd)))
 
 
 def step(cells=(), pseudos=(), generations=1, traces=True):

@@ -131,11 +131,19 @@ struct ffsga_cuda_instance_t {
     long long ev_cap = 0;
     // migration scratch
     DevBuf mg_keys0, mg_keys1, mg_idx0, mg_idx_a, mg_idx_b, mg_temp;
-    // timing
+    // timing: event pairs recorded around launches, resolved lazily (no sync in the timed path)
     bool timing = false;
     double t_ms[3] = {0, 0, 0};
     long long t_n[3] = {0, 0, 0};
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    struct Pending {
+        int which;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, st0 = nullptr, st1 = nullptr;
+    bool step_recorded = false;
+    DevBuf eval_total;  // evaluations performed by ffsga_cuda_step (device counter)
 
     size_t block() const { return (size_t)S * Jpad; }
     void use() const { CK(cudaSetDevice(device)); }
@@ -144,22 +152,48 @@ struct ffsga_cuda_instance_t {
         if (stream) cudaStreamDestroy(stream);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (st0) cudaEventDestroy(st0);
+        if (st1) cudaEventDestroy(st1);
+        for (auto& p : pending) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
     }
-    // brackets a launch with events when timing is enabled
+    cudaEvent_t take_event() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    // brackets a launch with events when timing is enabled (resolved by resolve_timing)
     template <typename F>
     void timed(int which, F&& f) {
         if (!timing) {
             f();
             return;
         }
-        CK(cudaEventRecord(ev0, stream));
+        Pending p{which, take_event(), take_event()};
+        CK(cudaEventRecord(p.a, stream));
         f();
-        CK(cudaEventRecord(ev1, stream));
-        CK(cudaEventSynchronize(ev1));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev0, ev1));
-        t_ms[which] += ms;
-        t_n[which] += 1;
+        CK(cudaEventRecord(p.b, stream));
+        pending.push_back(p);
+    }
+    void resolve_timing() {
+        for (auto& p : pending) {
+            CK(cudaEventSynchronize(p.b));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            t_ms[p.which] += ms;
+            t_n[p.which] += 1;
+            pool.push_back(p.a);
+            pool.push_back(p.b);
+        }
+        pending.clear();
     }
 };
 
@@ -375,7 +409,11 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&I->ev0));
         CK(cudaEventCreate(&I->ev1));
+        CK(cudaEventCreate(&I->st0));
+        CK(cudaEventCreate(&I->st1));
         I->wl_count.alloc(sizeof(long long));
+        I->eval_total.alloc(sizeof(unsigned long long));
+        CK(cudaMemset(I->eval_total.p, 0, sizeof(unsigned long long)));
         *out = hold.release();
     });
 }
@@ -876,6 +914,54 @@ int ffsga_cuda_cellular_best(ffsga_cuda_cellular c, int* index, double* fit, dou
     });
 }
 
+int ffsga_cuda_cellular_candidate(ffsga_cuda_cellular c, int index, uint64_t stream_state, int32_t* genes,
+                                  double* fit, double* obj, int* replaced, uint64_t* draws_used) {
+    return guard([&] {
+        if (!c || !genes || !fit || !obj || !replaced) fail(FFSGA_ERR_ARG, "cellular_candidate: null pointer");
+        if (index < 0 || index >= c->n) fail(FFSGA_ERR_CONTRACT, "cell index out of range");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        ffsga_cuda_instance_t* I = c->inst;
+        I->use();
+        const int q = c->parity();
+        ensure_eval_staging(I, 1);
+        DevBuf draws;
+        draws.alloc(sizeof(unsigned long long));
+        CK(launch_cell_candidate(I->d, c->d, index, stream_state, q, I->ev_rows.as<uint8_t>(), draws.as<unsigned long long>(),
+                                 I->stream));
+        g_launches += 1;
+        eval_rows(I, I->ev_rows.as<uint8_t>(), 1, I->ev_obj.as<double>(), I->ev_fit.as<double>(), nullptr, nullptr, true);
+        const unsigned long long code = read_error(I);
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        double cf = 0, co = 0, f0 = 0, o0 = 0;
+        unsigned long long used = 0;
+        CK(cudaMemcpy(&cf, I->ev_fit.p, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&co, I->ev_obj.p, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&f0, c->fit.as<double>() + (size_t)q * c->n + index, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&o0, c->obj.as<double>() + (size_t)q * c->n + index, sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&used, draws.p, sizeof(used), cudaMemcpyDeviceToHost));
+        const bool rep = cf > f0;  // strict improvement (cellular.cpp:153)
+        const size_t L = (size_t)I->J * I->S;
+        DevBuf out, didx;
+        out.alloc(sizeof(int32_t) * L);
+        const uint8_t* src = I->ev_rows.as<uint8_t>();
+        long long row = 0;
+        if (!rep) {
+            src = c->genes.as<uint8_t>();
+            row = cell_storage_index(c)[index];
+        }
+        std::vector<long long> idx{row};
+        upload(didx, idx);
+        CK(launch_rows_to_int(I->d, src, (long long)I->block(), didx.as<long long>(), out.as<int32_t>(), 1, I->stream));
+        g_launches += 1;
+        CK(cudaMemcpyAsync(genes, out.p, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        *fit = rep ? cf : f0;
+        *obj = rep ? co : o0;
+        *replaced = rep ? 1 : 0;
+        if (draws_used) *draws_used = used;
+    });
+}
+
 int ffsga_cuda_cellular_install(ffsga_cuda_cellular c, int index, const int32_t* genes, double fit, double obj) {
     return guard([&] {
         if (!c || !genes) fail(FFSGA_ERR_ARG, "null pointer");
@@ -1038,6 +1124,25 @@ int ffsga_cuda_pseudo_archive(ffsga_cuda_pseudo p, double* fit, double* obj, uin
     });
 }
 
+int ffsga_cuda_pseudo_archive_genes(ffsga_cuda_pseudo p, int32_t* genes) {
+    return guard([&] {
+        if (!p || !genes) fail(FFSGA_ERR_ARG, "null pointer");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        ffsga_cuda_instance_t* I = p->inst;
+        I->use();
+        const size_t L = (size_t)I->J * I->S;
+        DevBuf rows, out;
+        rows.alloc(I->block());
+        out.alloc(sizeof(int32_t) * L);
+        CK(launch_unpack_rows(I->d, p->archive.as<unsigned long long>(), nullptr, rows.as<uint8_t>(), (long long)I->block(),
+                              nullptr, 1, I->stream));
+        CK(launch_rows_to_int(I->d, rows.as<uint8_t>(), (long long)I->block(), nullptr, out.as<int32_t>(), 1, I->stream));
+        g_launches += 2;
+        CK(cudaMemcpyAsync(genes, out.p, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
 int ffsga_cuda_pseudo_install(ffsga_cuda_pseudo p, int index, const uint8_t* bits, double fit, double obj) {
     return guard([&] {
         if (!p || !bits) fail(FFSGA_ERR_ARG, "null pointer");
@@ -1123,6 +1228,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         wl.count = I->wl_count.as<long long>();
         wl.scratch = I->wl_scratch.as<uint8_t>();
         wl.scratch0 = n_cells;
+        wl.total = I->eval_total.as<unsigned long long>();
         const CellIsland* cdev = I->cell_desc.as<CellIsland>();
         const PseudoIsland* pdev = I->pseudo_desc.as<PseudoIsland>();
         EvalItems W{};
@@ -1130,12 +1236,15 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         W.ptrs = wl.ptrs;
         W.obj = wl.obj;
         W.fit = wl.fit;
+        CK(cudaEventRecord(I->st0, I->stream));
         for (int g = 0; g < generations; ++g) {
             I->timed(1, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, pdev, np, n_pairs, wl, I->stream)); });
             I->timed(0, [&] { CK(launch_eval(I->d, I->ec, W, cap, I->sm_count, false, I->stream)); });
             I->timed(2, [&] { CK(launch_commit(I->d, cdev, nc, pdev, np, wl, I->stream)); });
             g_launches += 3 + (nc > 0 ? 1 : 0) + (np > 0 ? 1 : 0);
         }
+        CK(cudaEventRecord(I->st1, I->stream));
+        I->step_recorded = true;
         for (int i = 0; i < nc; ++i) {
             if (trace_c)
                 CK(cudaMemcpyAsync(trace_c + (size_t)i * generations, cells[i]->trace.p, sizeof(double) * generations,
@@ -1217,6 +1326,176 @@ int ffsga_cuda_migrate_pseudo_to_cellular(ffsga_cuda_pseudo from, ffsga_cuda_cel
     });
 }
 
+int ffsga_cuda_cellular_export(ffsga_cuda_cellular c, int k, int32_t* genes, double* fit, double* obj) {
+    return guard([&] {
+        if (!c || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
+        if (k < 0 || k > c->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = c->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        const int q = c->parity();
+        sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_a);
+        std::vector<long long> best(k);
+        CK(cudaMemcpyAsync(best.data(), I->mg_idx_a.p, sizeof(long long) * k, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        std::vector<long long> storage = cell_storage_index(c);
+        std::vector<long long> src(k);
+        for (int i = 0; i < k; ++i) src[i] = storage[best[i]];
+        DevBuf dsrc, out;
+        upload(dsrc, src);
+        const size_t L = (size_t)I->J * I->S;
+        out.alloc(sizeof(int32_t) * L * k);
+        CK(launch_rows_to_int(I->d, c->genes.as<uint8_t>(), (long long)I->block(), dsrc.as<long long>(), out.as<int32_t>(), k,
+                              I->stream));
+        g_launches += 1;
+        CK(cudaMemcpyAsync(genes, out.p, sizeof(int32_t) * L * k, cudaMemcpyDeviceToHost, I->stream));
+        std::vector<double> f(c->n), o(c->n);
+        CK(cudaMemcpyAsync(f.data(), c->fit.as<double>() + (size_t)q * c->n, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(o.data(), c->obj.as<double>() + (size_t)q * c->n, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        for (int i = 0; i < k; ++i) {
+            fit[i] = f[best[i]];
+            obj[i] = o[best[i]];
+        }
+    });
+}
+
+int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* fit, double* obj) {
+    return guard([&] {
+        if (!p || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
+        if (k < 0 || k > p->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = p->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_a);
+        std::vector<long long> best(k);
+        CK(cudaMemcpyAsync(best.data(), I->mg_idx_a.p, sizeof(long long) * k, cudaMemcpyDeviceToHost, I->stream));
+        std::vector<double> f(p->n), o(p->n);
+        CK(cudaMemcpyAsync(f.data(), p->fit.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(o.data(), p->obj.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        const int W = I->words, nb = I->total_bits;
+        std::vector<unsigned long long> w(W);
+        for (int i = 0; i < k; ++i) {
+            CK(cudaMemcpy(w.data(), p->words.as<unsigned long long>() + (size_t)best[i] * W, sizeof(unsigned long long) * W,
+                          cudaMemcpyDeviceToHost));
+            unpack_host_bits(w.data(), nb, bits + (size_t)i * nb);
+            fit[i] = f[best[i]];
+            obj[i] = o[best[i]];
+        }
+    });
+}
+
+int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits, const double* fit, const double* obj) {
+    return guard([&] {
+        if (!c || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
+        if (k < 0 || k > c->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = c->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        const int q = c->parity();
+        sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_b);
+        std::vector<long long> order(c->n);
+        CK(cudaMemcpyAsync(order.data(), I->mg_idx_b.p, sizeof(long long) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        std::vector<long long> storage = cell_storage_index(c);
+        const int W = I->words;
+        std::vector<unsigned long long> words((size_t)W * k), w;
+        std::vector<long long> dst(k);
+        for (int i = 0; i < k; ++i) {
+            pack_host_bits(bits + (size_t)i * I->total_bits, I->total_bits, W, w);
+            std::copy(w.begin(), w.end(), words.begin() + (size_t)i * W);
+            dst[i] = storage[order[c->n - 1 - i]];
+        }
+        DevBuf dw, ddst;
+        upload(dw, words);
+        upload(ddst, dst);
+        CK(launch_unpack_rows(I->d, dw.as<unsigned long long>(), nullptr, c->genes.as<uint8_t>(), (long long)I->block(),
+                              ddst.as<long long>(), k, I->stream));
+        g_launches += 1;
+        std::vector<double> f(c->n), o(c->n);
+        double* df = c->fit.as<double>() + (size_t)q * c->n;
+        double* dob = c->obj.as<double>() + (size_t)q * c->n;
+        CK(cudaMemcpyAsync(f.data(), df, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(o.data(), dob, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        for (int i = 0; i < k; ++i) {
+            f[order[c->n - 1 - i]] = fit[i];
+            o[order[c->n - 1 - i]] = obj[i];
+        }
+        CK(cudaMemcpy(df, f.data(), sizeof(double) * c->n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dob, o.data(), sizeof(double) * c->n, cudaMemcpyHostToDevice));
+        refresh_stats(c, nullptr, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_pseudo_import(ffsga_cuda_pseudo p, int k, const int32_t* genes, const double* fit, const double* obj) {
+    return guard([&] {
+        if (!p || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
+        if (k < 0 || k > p->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        if (k == 0) return;
+        ffsga_cuda_instance_t* I = p->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
+        I->use();
+        sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_b);
+        std::vector<long long> order(p->n);
+        CK(cudaMemcpyAsync(order.data(), I->mg_idx_b.p, sizeof(long long) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        const size_t L = (size_t)I->J * I->S;
+        DevBuf gi, rows, ddst;
+        gi.alloc(sizeof(int32_t) * L * k);
+        rows.alloc(I->block() * k);
+        CK(cudaMemcpy(gi.p, genes, sizeof(int32_t) * L * k, cudaMemcpyHostToDevice));
+        std::vector<long long> dst(k);
+        for (int i = 0; i < k; ++i) dst[i] = order[p->n - 1 - i];
+        upload(ddst, dst);
+        CK(launch_rows_from_int(I->d, gi.as<int32_t>(), nullptr, rows.as<uint8_t>(), k, I->stream));
+        CK(launch_pack_bits(I->d, rows.as<uint8_t>(), (long long)I->block(), nullptr, p->words.as<unsigned long long>(),
+                            ddst.as<long long>(), k, false, I->dBitStage.as<uint16_t>(), I->stream));
+        g_launches += 2;
+        std::vector<double> f(p->n), o(p->n);
+        CK(cudaMemcpyAsync(f.data(), p->fit.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(o.data(), p->obj.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
+        IslandState s = read_state(I, p->st);
+        int take = -1;
+        double af = s.arch_fit;
+        for (int i = 0; i < k; ++i) {
+            f[dst[i]] = fit[i];
+            o[dst[i]] = obj[i];
+            if (fit[i] > af) {  // consider_for_archive in install order (pseudo.cpp:98-113)
+                af = fit[i];
+                take = i;
+            }
+        }
+        CK(cudaMemcpy(p->fit.p, f.data(), sizeof(double) * p->n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->obj.p, o.data(), sizeof(double) * p->n, cudaMemcpyHostToDevice));
+        if (take >= 0) {
+            s.arch_fit = fit[take];
+            s.arch_obj = obj[take];
+            CK(cudaMemcpy(p->st.p, &s, sizeof(s), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(p->archive.p, p->words.as<unsigned long long>() + (size_t)dst[take] * I->words,
+                          sizeof(unsigned long long) * I->words, cudaMemcpyDeviceToDevice));
+        }
+        refresh_stats(nullptr, p, 0);
+        CK(cudaStreamSynchronize(I->stream));
+    });
+}
+
+int ffsga_cuda_last_step_ms(ffsga_cuda_instance inst, float* ms) {
+    return guard([&] {
+        if (!inst || !ms) fail(FFSGA_ERR_ARG, "null pointer");
+        if (!inst->step_recorded) fail(FFSGA_ERR_CONTRACT, "no step recorded");
+        inst->use();
+        CK(cudaEventSynchronize(inst->st1));
+        CK(cudaEventElapsedTime(ms, inst->st0, inst->st1));
+    });
+}
+
 int ffsga_cuda_set_timing(ffsga_cuda_instance inst, int enabled) {
     return guard([&] {
         if (!inst) fail(FFSGA_ERR_ARG, "null instance");
@@ -1227,14 +1506,32 @@ int ffsga_cuda_set_timing(ffsga_cuda_instance inst, int enabled) {
 int ffsga_cuda_timing(ffsga_cuda_instance inst, int which, double* ms, int64_t* launches) {
     return guard([&] {
         if (!inst || which < 0 || which > 2) fail(FFSGA_ERR_ARG, "timing: bad argument");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        inst->resolve_timing();
         if (ms) *ms = inst->t_ms[which];
         if (launches) *launches = inst->t_n[which];
+    });
+}
+
+int ffsga_cuda_evaluations(ffsga_cuda_instance inst, int64_t* count) {
+    return guard([&] {
+        if (!inst || !count) fail(FFSGA_ERR_ARG, "null pointer");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        unsigned long long v = 0;
+        CK(cudaMemcpyAsync(&v, inst->eval_total.p, sizeof(v), cudaMemcpyDeviceToHost, inst->stream));
+        CK(cudaStreamSynchronize(inst->stream));
+        *count = (int64_t)v;
     });
 }
 
 int ffsga_cuda_reset_timing(ffsga_cuda_instance inst) {
     return guard([&] {
         if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        inst->resolve_timing();
         for (int i = 0; i < 3; ++i) {
             inst->t_ms[i] = 0;
             inst->t_n[i] = 0;

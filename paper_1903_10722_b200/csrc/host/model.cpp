@@ -1,0 +1,345 @@
+// model.cpp -- instance helpers, generator, genome views and the device-backed decoder API.
+//
+// Host code here is bookkeeping (validation, instance generation, representation helpers);
+// every chromosome evaluation and schedule decode goes through the C ABI to the sm_100a
+// kernels (K1/K7).  Reference behaviour followed: proj/src/model.cpp, generator.cpp,
+// chromosome.cpp (same contracts, messages and arithmetic order).
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+
+#include "ffsga/chromosome.hpp"
+#include "ffsga/device.hpp"
+#include "ffsga/errors.hpp"
+#include "ffsga/generator.hpp"
+#include "ffsga/model.hpp"
+#include "ffsga/rng.hpp"
+#include "ffsga_cuda.h"
+
+namespace ffsga {
+
+void check_status(int status) {
+    if (status == FFSGA_OK) return;
+    const std::string msg = ffsga_cuda_last_error();
+    switch (status) {
+        case FFSGA_ERR_CONTRACT: throw ContractError(msg);
+        case FFSGA_ERR_CONFIG: throw ConfigError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+// ------------------------------------------------------------------------------ instance
+void Instance::finalize() {
+    stage_offset.resize(machines_per_stage.size() + 1);
+    stage_offset[0] = 0;
+    std::partial_sum(machines_per_stage.begin(), machines_per_stage.end(), stage_offset.begin() + 1);
+    machines_total = stage_offset.back();
+}
+
+void Instance::validate() const {
+    // structural checks in the order of proj/src/model.cpp:18-47
+    auto bad = [](const std::string& what) { throw ContractError("instance: " + what); };
+    if (num_jobs < 1) bad("num_jobs must be >= 1");
+    if (num_stages < 2) bad("num_stages must be >= 2");
+    if ((int)machines_per_stage.size() != num_stages) bad("machines_per_stage length must equal num_stages");
+    if (std::any_of(machines_per_stage.begin(), machines_per_stage.end(), [](int m) { return m < 1; }))
+        bad("every stage needs at least one machine");
+    if (std::none_of(machines_per_stage.begin(), machines_per_stage.end(), [](int m) { return m >= 2; }))
+        bad("at least one stage must have more than one machine");
+    const int total = std::accumulate(machines_per_stage.begin(), machines_per_stage.end(), 0);
+    if ((int)stage_offset.size() != num_stages + 1 || machines_total != total)
+        bad("layout helpers stale, call finalize()");
+    if ((long long)proc.size() != (long long)num_jobs * machines_total) bad("proc_time size mismatch");
+    if (std::any_of(proc.begin(), proc.end(), [](double p) { return !(p > 0.0); }))
+        bad("processing times must be positive");
+    if ((int)release.size() != num_jobs) bad("release length must equal num_jobs");
+    if ((int)due.size() != num_jobs) bad("due length must equal num_jobs");
+    for (int j = 0; j < num_jobs; ++j) {
+        if (!(release[j] >= 0.0)) bad("release times must be >= 0");
+        if (!(due[j] >= release[j])) bad("due time before release of job " + std::to_string(j));
+    }
+    if (!(weight >= 0.0)) bad("weight must be >= 0");
+}
+
+GeneCoords gene_index_map(int gene, int num_stages, int num_jobs) {
+    if (num_stages < 1) throw ContractError("gene_index_map: num_stages must be >= 1");
+    if (gene < 0 || gene >= num_jobs * num_stages) throw ContractError("gene_index_map: gene index out of range");
+    return GeneCoords{gene / num_stages, gene % num_stages};
+}
+
+double mean_job_load(const Instance& inst, int job) {
+    double load = 0.0;
+    for (int s = 0; s < inst.num_stages; ++s) {
+        const int m = inst.machines_per_stage[s];
+        const double* row = inst.proc.data() + inst.proc_index(job, s, 0);
+        double stage_sum = 0.0;
+        for (int k = 0; k < m; ++k) stage_sum += row[k];
+        load += stage_sum / m;
+    }
+    return load;
+}
+
+double mean_total_load(const Instance& inst) {
+    double load = 0.0;
+    for (int j = 0; j < inst.num_jobs; ++j) load += mean_job_load(inst, j);
+    return load;
+}
+
+double estimate_emax(const Instance& inst) {
+    // H = latest release + every (job, stage) at its slowest machine; the bound charges every
+    // job tardiness up to H (model.cpp:167-181).  Same summation order.
+    double horizon = 0.0;
+    for (double r : inst.release) horizon = (horizon < r) ? r : horizon;
+    for (int j = 0; j < inst.num_jobs; ++j)
+        for (int s = 0; s < inst.num_stages; ++s) {
+            const double* row = inst.proc.data() + inst.proc_index(j, s, 0);
+            double slowest = 0.0;
+            for (int k = 0; k < inst.machines_per_stage[s]; ++k) slowest = (slowest < row[k]) ? row[k] : slowest;
+            horizon += slowest;
+        }
+    double bound = 0.0;
+    for (double d : inst.due) {
+        const double late = horizon - d;
+        bound += (0.0 < late) ? late : 0.0;
+    }
+    return inst.weight * bound + horizon;
+}
+
+// ------------------------------------------------------------------------------ device instances
+namespace {
+
+int default_device() {
+    for (const char* var : {"FFSGA_DEVICE", "LOCAL_RANK"}) {
+        if (const char* v = std::getenv(var)) return std::atoi(v);
+    }
+    return 0;
+}
+
+struct Entry {
+    Instance copy;
+    double emax;
+    std::weak_ptr<DeviceInstance> dev;
+};
+
+bool same(const Instance& a, const Instance& b) {
+    return a.num_jobs == b.num_jobs && a.num_stages == b.num_stages && a.machines_per_stage == b.machines_per_stage &&
+           a.weight == b.weight && a.proc == b.proc && a.release == b.release && a.due == b.due;
+}
+
+std::uint64_t digest(const Instance& inst, double emax) {
+    std::uint64_t h = 1469598103934665603ULL;
+    auto mixin = [&](const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ULL;
+    };
+    mixin(&inst.num_jobs, sizeof(int));
+    mixin(&inst.num_stages, sizeof(int));
+    mixin(inst.machines_per_stage.data(), sizeof(int) * inst.machines_per_stage.size());
+    mixin(&inst.weight, sizeof(double));
+    mixin(&emax, sizeof(double));
+    mixin(inst.release.data(), sizeof(double) * inst.release.size());
+    mixin(inst.due.data(), sizeof(double) * inst.due.size());
+    mixin(inst.proc.data(), sizeof(double) * inst.proc.size());
+    return h;
+}
+
+std::mutex g_registry_mu;
+std::multimap<std::uint64_t, Entry> g_registry;
+
+}  // namespace
+
+DeviceInstance::DeviceInstance(const Instance& inst, double emax) : emax_(emax) {
+    if ((int)inst.machines_per_stage.size() != inst.num_stages || (int)inst.release.size() != inst.num_jobs ||
+        (int)inst.due.size() != inst.num_jobs ||
+        (long long)inst.proc.size() != (long long)inst.num_jobs * inst.machines_total)
+        throw ContractError("instance: layout helpers stale, call finalize()");
+    ffsga_cuda_instance h = nullptr;
+    check_status(ffsga_cuda_instance_create(default_device(), inst.num_jobs, inst.num_stages,
+                                            inst.machines_per_stage.data(), inst.proc.data(), inst.release.data(),
+                                            inst.due.data(), inst.weight, emax, &h));
+    handle_ = h;
+}
+
+DeviceInstance::~DeviceInstance() {
+    if (handle_) ffsga_cuda_instance_destroy(static_cast<ffsga_cuda_instance>(handle_));
+}
+
+std::shared_ptr<DeviceInstance> DeviceInstance::get(const Instance& inst, double emax) {
+    const std::uint64_t key = digest(inst, emax);
+    std::lock_guard<std::mutex> lk(g_registry_mu);
+    auto range = g_registry.equal_range(key);
+    for (auto it = range.first; it != range.second;) {
+        if (auto dev = it->second.dev.lock()) {
+            if (it->second.emax == emax && same(it->second.copy, inst)) return dev;
+            ++it;
+        } else {
+            it = g_registry.erase(it);
+        }
+    }
+    auto dev = std::make_shared<DeviceInstance>(inst, emax);
+    g_registry.emplace(key, Entry{inst, emax, dev});
+    return dev;
+}
+
+// ------------------------------------------------------------------------------ decoder API
+Schedule decode(const Instance& inst, std::span<const int> assignment) {
+    if ((int)assignment.size() != inst.num_genes())
+        throw ContractError("decode: assignment length must be num_jobs * num_stages");
+    auto dev = DeviceInstance::get(inst, 0.0);
+    Schedule sched;
+    sched.num_jobs = inst.num_jobs;
+    sched.num_stages = inst.num_stages;
+    sched.machine.resize(inst.num_genes());
+    sched.start.resize(inst.num_genes());
+    sched.completion.resize(inst.num_genes());
+    check_status(ffsga_cuda_decode(static_cast<ffsga_cuda_instance>(dev->handle()), assignment.data(),
+                                   sched.machine.data(), sched.start.data(), sched.completion.data(), nullptr));
+    return sched;
+}
+
+ObjectiveReport evaluate(const Instance& inst, const Schedule& sched, double emax) {
+    // report_from_completions over the last-stage completions (model.cpp:107-120, 141-149)
+    if (sched.num_jobs != inst.num_jobs || sched.num_stages != inst.num_stages)
+        throw ContractError("evaluate: schedule shape does not match instance");
+    if (!(emax >= 0.0)) throw ContractError("evaluate: emax must be >= 0");
+    ObjectiveReport rep;
+    rep.emax_used = emax;
+    for (int j = 0; j < inst.num_jobs; ++j) {
+        const double c = sched.completion[sched.at(j, inst.num_stages - 1)];
+        rep.makespan = (rep.makespan < c) ? c : rep.makespan;
+        const double late = c - inst.due[j];
+        rep.total_tardiness += (0.0 < late) ? late : 0.0;
+    }
+    rep.objective = inst.weight * rep.total_tardiness + rep.makespan;
+    const double slack = emax - rep.objective;
+    rep.fitness = (slack < 0.0) ? 0.0 : slack;
+    return rep;
+}
+
+Evaluator::Evaluator(const Instance& inst, double emax)
+    : inst_(&inst), emax_(emax), dev_(DeviceInstance::get(inst, emax)) {}
+
+Evaluator::~Evaluator() = default;
+
+ObjectiveReport Evaluator::score(std::span<const int> assignment) {
+    if ((int)assignment.size() != inst_->num_genes())
+        throw ContractError("decode: assignment length must be num_jobs * num_stages");
+    ObjectiveReport r;
+    r.emax_used = emax_;
+    check_status(ffsga_cuda_evaluate(static_cast<ffsga_cuda_instance>(dev_->handle()), assignment.data(), 1,
+                                     &r.objective, &r.fitness, &r.makespan, &r.total_tardiness));
+    return r;
+}
+
+std::vector<ObjectiveReport> Evaluator::score_batch(std::span<const int> assignments) {
+    const int L = inst_->num_genes();
+    if (L == 0 || assignments.size() % L != 0)
+        throw ContractError("score_batch: size must be a multiple of num_jobs * num_stages");
+    const int64_t n = (int64_t)(assignments.size() / L);
+    std::vector<double> obj(n), fit(n), mk(n), td(n);
+    check_status(ffsga_cuda_evaluate(static_cast<ffsga_cuda_instance>(dev_->handle()), assignments.data(), n,
+                                     obj.data(), fit.data(), mk.data(), td.data()));
+    std::vector<ObjectiveReport> out(n);
+    for (int64_t i = 0; i < n; ++i) out[i] = ObjectiveReport{mk[i], td[i], obj[i], fit[i], emax_};
+    return out;
+}
+
+// ------------------------------------------------------------------------------ generator
+Instance generate(const GenParams& params) {
+    // draw order (generator.cpp:11-48): processing times job -> stage -> machine, then one
+    // release per job, then one slack factor per job
+    if (params.num_jobs < 1) throw ConfigError("generate: num_jobs must be >= 1");
+    if (params.num_stages < 2) throw ConfigError("generate: num_stages must be >= 2");
+    if ((int)params.machines_per_stage.size() != params.num_stages)
+        throw ConfigError("generate: machines_per_stage length must equal num_stages");
+    if (!(params.weight >= 0.0)) throw ConfigError("generate: weight must be >= 0");
+    Instance inst;
+    inst.num_jobs = params.num_jobs;
+    inst.num_stages = params.num_stages;
+    inst.machines_per_stage = params.machines_per_stage;
+    inst.weight = params.weight;
+    inst.finalize();
+    Rng rng(params.seed);
+    inst.proc.assign((size_t)inst.num_jobs * inst.machines_total, 0.0);
+    for (double& p : inst.proc) {  // job-major flat order == job, stage, machine order
+        const double v = rng.next_uniform(1.0, 5.0);
+        p = params.integer_times ? std::round(v) : v;
+    }
+    const double load = mean_total_load(inst);
+    inst.release.resize(inst.num_jobs);
+    for (double& r : inst.release) r = rng.next_uniform(0.0, load);
+    inst.due.resize(inst.num_jobs);
+    for (int j = 0; j < inst.num_jobs; ++j) {
+        const double slack = rng.next_uniform(0.0, 2.0);
+        inst.due[j] = inst.release[j] + mean_job_load(inst, j) * (1.0 + slack);
+    }
+    inst.validate();
+    return inst;
+}
+
+// ------------------------------------------------------------------------------ genome views
+BitLayout BitLayout::for_instance(const Instance& inst) {
+    BitLayout lay;
+    lay.num_jobs = inst.num_jobs;
+    lay.num_stages = inst.num_stages;
+    lay.machines_per_stage = inst.machines_per_stage;
+    lay.bits_per_stage.resize(inst.num_stages);
+    lay.stage_bit_offset.assign(inst.num_stages + 1, 0);
+    for (int s = 0; s < inst.num_stages; ++s) {
+        const unsigned span = static_cast<unsigned>(inst.machines_per_stage[s]) - 1u;
+        lay.bits_per_stage[s] = std::max(1, static_cast<int>(std::bit_width(span)));
+        lay.stage_bit_offset[s + 1] = lay.stage_bit_offset[s] + lay.bits_per_stage[s];
+    }
+    lay.bits_per_job = lay.stage_bit_offset.back();
+    lay.total_bits = lay.num_jobs * lay.bits_per_job;
+    return lay;
+}
+
+BitChromosome int_to_bits(const IntChromosome& c, const BitLayout& layout) {
+    if ((int)c.genes.size() != layout.num_genes()) throw ContractError("int_to_bits: gene count does not match layout");
+    BitChromosome out;
+    out.bits.assign(layout.total_bits, 0);
+    for (int g = 0; g < layout.num_genes(); ++g) {
+        const int width = layout.bits_per_stage[g % layout.num_stages];
+        uint8_t* slot = out.bits.data() + layout.gene_offset(g);
+        const unsigned v = static_cast<unsigned>(c.genes[g]);
+        for (int b = width - 1, k = 0; b >= 0; --b, ++k) slot[k] = static_cast<uint8_t>((v >> b) & 1u);  // MSB first
+    }
+    return out;
+}
+
+IntChromosome bits_to_int(const BitChromosome& b, const BitLayout& layout) {
+    if ((int)b.bits.size() != layout.total_bits) throw ContractError("bits_to_int: bit count does not match layout");
+    IntChromosome out;
+    out.genes.resize(layout.num_genes());
+    for (int g = 0; g < layout.num_genes(); ++g) {
+        const int s = g % layout.num_stages;
+        const uint8_t* slot = b.bits.data() + layout.gene_offset(g);
+        unsigned v = 0;
+        for (int k = 0; k < layout.bits_per_stage[s]; ++k) v = (v << 1) | slot[k];
+        out.genes[g] = static_cast<int>(v % static_cast<unsigned>(layout.machines_per_stage[s]));
+    }
+    return out;
+}
+
+BitChromosome complement(const BitChromosome& b) {
+    BitChromosome out;
+    out.bits.resize(b.bits.size());
+    std::transform(b.bits.begin(), b.bits.end(), out.bits.begin(), [](uint8_t x) { return (uint8_t)(x ^ 1u); });
+    return out;
+}
+
+IntChromosome random_int_chromosome(const Instance& inst, Rng& rng) {
+    IntChromosome c;
+    c.genes.resize(inst.num_genes());
+    for (int g = 0; g < inst.num_genes(); ++g) c.genes[g] = rng.next_index(inst.machines_per_stage[g % inst.num_stages]);
+    return c;
+}
+
+}  // namespace ffsga

@@ -441,22 +441,20 @@ constexpr int kMutChunk = 8;  // draws per lane per window of the mutation strea
 // (one coin per gene plus one index draw per mutated gene, 148-150) is parsed warp-parallel:
 // draw k of the cell stream is mix(seed + (k+1) gamma), so each lane evaluates its slice of
 // the stream and a warp scan of the 2-state {coin, index} automaton assigns gene indices.
-__global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland* __restrict__ isl,
-                                                     int n_islands, long long n_cells, WorkList wl) {
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n_cells) return;
-    int ii = 0;
-    while (ii + 1 < n_islands && isl[ii + 1].cell0 <= warp) ++ii;
-    const CellIsland& C = isl[ii];
-    const int cell = (int)(warp - C.cell0);
+__device__ __forceinline__ unsigned long long shfl_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, v, off);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+
+// One cell, one warp: writes the child rows and returns the number of stream draws consumed.
+__device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, int cell, unsigned long long cs,
+                                         const double* __restrict__ fit, const uint8_t* __restrict__ selq,
+                                         uint8_t* __restrict__ child, int lane) {
     const int n = C.n;
-    const unsigned long long gen = C.st->gen;
-    const int q = (int)(gen & 1ull);
-    const double* fit = C.fit + (size_t)q * n;
-    const uint8_t* selq = C.sel + (size_t)q * n;
-    const unsigned long long gen_seed = derive_seed(C.seed, gen + 1ull);  // cellular.cpp:167
-    const unsigned long long cs = derive_seed(gen_seed, (unsigned long long)cell);  // :171
     const int L = I.J * I.S;
     unsigned long long k = 0;
     const int npc = C.npc;
@@ -488,7 +486,6 @@ __global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland*
     const size_t block = (size_t)I.S * I.Jpad;
     const uint8_t* g1 = C.genes + ((size_t)selq[p1] * n + p1) * block;
     const uint8_t* g2 = C.genes + ((size_t)selq[p2] * n + p2) * block;
-    uint8_t* child = C.genes + ((size_t)(1 - selq[cell]) * n + cell) * block;
 
     // two-point crossover on the job-major index i = j*S + s (cellular.cpp:136-146)
     const int vec_per_row = I.Jpad / 16;
@@ -523,6 +520,7 @@ __global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland*
     // mutation (cellular.cpp:148-150)
     const unsigned long long thr = C.thr_mu;
     unsigned long long pos = k;
+    unsigned long long end = k;
     long long coins_before = 0;
     bool st_coin = true;
     while (coins_before < L || (coins_before == L && !st_coin)) {
@@ -573,8 +571,10 @@ __global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland*
 #pragma unroll
         for (int t = 0; t < kMutChunk; ++t) {
             if (st) {
+                const int bit = (tb >> t) & 1;
+                if (g == L - 1) end = p0 + t + 1 + (unsigned long long)bit;
                 ++g;
-                st = !((tb >> t) & 1);
+                st = !bit;
             } else {
                 const long long gene = g - 1;
                 if (gene < L) {
@@ -591,7 +591,41 @@ __global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland*
         st_coin = st_coin ? lF1 : lF0;
         pos += 32ull * kMutChunk;
     }
+    return shfl_max_u64(end);
+}
+
+// compute_cell (cellular.cpp:116-150) for one cell per warp.  The serial prefix (tournaments,
+// crossover coin and cut points) is replayed redundantly by every lane; the mutation loop
+// (one coin per gene plus one index draw per mutated gene, 148-150) is parsed warp-parallel:
+// draw k of the cell stream is mix(seed + (k+1) gamma), so each lane evaluates its slice of
+// the stream and a warp scan of the 2-state {coin, index} automaton assigns gene indices.
+__global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland* __restrict__ isl,
+                                                     int n_islands, long long n_cells, WorkList wl) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_cells) return;
+    int ii = 0;
+    while (ii + 1 < n_islands && isl[ii + 1].cell0 <= warp) ++ii;
+    const CellIsland& C = isl[ii];
+    const int cell = (int)(warp - C.cell0);
+    const int n = C.n;
+    const unsigned long long gen = C.st->gen;
+    const int q = (int)(gen & 1ull);
+    const uint8_t* selq = C.sel + (size_t)q * n;
+    const unsigned long long gen_seed = derive_seed(C.seed, gen + 1ull);  // cellular.cpp:167
+    const unsigned long long cs = derive_seed(gen_seed, (unsigned long long)cell);  // :171
+    uint8_t* child = C.genes + ((size_t)(1 - selq[cell]) * n + cell) * ((size_t)I.S * I.Jpad);
+    breed_cell(I, C, cell, cs, C.fit + (size_t)q * n, selq, child, lane);
     if (lane == 0) wl.ptrs[C.item0 + cell] = child;
+}
+
+// cell_candidate (cellular.cpp:157-162) on an explicit stream: child rows into `out`.
+__global__ void k_cell_candidate(DevInst I, CellIsland C, int cell, unsigned long long cs, int q, uint8_t* out,
+                                 unsigned long long* draws) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long used =
+        breed_cell(I, C, cell, cs, C.fit + (size_t)q * C.n, C.sel + (size_t)q * C.n, out, lane);
+    if (lane == 0) *draws = used;
 }
 
 // ---------------------------------------------------------------------------- K4 pseudo breed
@@ -691,6 +725,7 @@ __global__ void __launch_bounds__(1024) k_commit(DevInst I, const CellIsland* __
     // mode 0: refresh best only; 1: commit one generation; 2: pseudo init (archive over all)
     const int advance = mode == 1;
     const int b = blockIdx.x;
+    if (advance && b == 0 && threadIdx.x == 0 && wl.total) atomicAdd(wl.total, (unsigned long long)*wl.count);
     if (b < nc) {
         const CellIsland& C = cells[b];
         const int n = C.n;
@@ -991,6 +1026,12 @@ cudaError_t launch_migrate_p2c(const DevInst& I, const PseudoIsland& p, const Ce
                                const long long* worst_c, int k, int parity, cudaStream_t st) {
     if (k <= 0) return cudaSuccess;
     k_migrate_p2c<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, p, c, best_p, worst_c, k, parity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cell_candidate(const DevInst& I, const CellIsland& c, int cell, unsigned long long stream_seed,
+                                  int parity, uint8_t* out, unsigned long long* draws, cudaStream_t st) {
+    k_cell_candidate<<<1, 32, 0, st>>>(I, c, cell, stream_seed, parity, out, draws);
     return cudaGetLastError();
 }
 

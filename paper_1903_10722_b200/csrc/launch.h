@@ -71,6 +71,7 @@ struct WorkList {
     long long* count;              // device counter
     uint8_t* scratch;              // pseudo children rows [cap_pseudo][S*Jpad]
     long long scratch0;            // item index of scratch row 0
+    unsigned long long* total;     // running count of evaluations (optional)
 };
 
 // ------------------------------------------------------------------ launchers
@@ -120,5 +121,8 @@ cudaError_t launch_migrate_p2c(const DevInst& I, const PseudoIsland& p, const Ce
                                const long long* best_p, const long long* worst_c, int k, int parity,
                                cudaStream_t st);
 cudaError_t launch_fill_seq(long long* idx, long long n, cudaStream_t st);
+// compute_cell of one cell on an explicit stream state (cellular.cpp:157-162)
+cudaError_t launch_cell_candidate(const DevInst& I, const CellIsland& c, int cell, unsigned long long stream_seed,
+                                  int parity, uint8_t* out, unsigned long long* draws, cudaStream_t st);
 
 }  // namespace ffsga_dev
