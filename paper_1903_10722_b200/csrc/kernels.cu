@@ -12,6 +12,9 @@
 // All fp64 arithmetic uses explicit round-to-nearest intrinsics (no FMA contraction) so results
 // are bit-identical to the reference built with -ffp-contract=off (proj/src/CMakeLists.txt:16).
 #include <cub/cub.cuh>
+#include <cuda_pipeline.h>
+
+#include <algorithm>
 
 #include "launch.h"
 
@@ -51,57 +54,78 @@ __device__ __forceinline__ void group_min_key(double& c, int& j) {
 }
 
 // ---------------------------------------------------------------------------- K1 decoder
+// Design: one group of G lanes per chromosome, lane m owns machine m of the
+// current stage; every group of a CTA advances stage by stage in lockstep (__syncthreads at
+// stage boundaries) so the CTA shares one stage slice of the processing-time table in L1.
+// Per-group shared memory: ready[J+1] fp64, link[J+1+G*G] u16, tail[G*G] u16, 2 gene rows.
+
+// Lexicographic (ready, job) minimum of NS list heads by a fixed tournament (depth log2 NS),
+// predicated selects only.  Jobs are distinct, so the minimum is unique whatever the tree shape.
+template <int NS>
+__device__ __forceinline__ void head_min(const double (&hr)[NS], const int (&hj)[NS], double& br, int& bj) {
+    double r[NS];
+    int j[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        r[k] = hr[k];
+        j[k] = hj[k];
+    }
+#pragma unroll
+    for (int stride = 1; stride < NS; stride *= 2) {
+#pragma unroll
+        for (int k = 0; k + stride < NS; k += 2 * stride) {
+            const bool lt = (r[k + stride] < r[k]) | ((r[k + stride] == r[k]) & (j[k + stride] < j[k]));
+            r[k] = lt ? r[k + stride] : r[k];
+            j[k] = lt ? j[k + stride] : j[k];
+        }
+    }
+    br = r[0];
+    bj = j[0];
+}
+
 // One stage of the list schedule for the group's chromosome (model.cpp:68-95).
 // Lane m (< Ms) merges the NS incoming per-source linked lists of jobs routed to machine m
 // (each list is sorted by completion because completions on one machine strictly increase),
 // which reproduces the (ready, job) sort of model.cpp:72-75 restricted to machine m, then runs
 // the machine's fp64 recurrence start = max(ready, avail), completion = start + p (84-87).
-// Each dispatched job is appended to the outgoing list (m -> gene of the next stage).
+// Each dispatched job is appended to the outgoing list (m -> gene of the next stage).  The
+// loop body is branch-free: out-of-range next-stage genes were flagged when the row arrived
+// and are resolved after the stage (they only ever land in lists nobody reads).
 template <int G, int NS, bool SCHED>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                            int m, bool work, double* __restrict__ ready,
                                            uint16_t* __restrict__ nxt, uint16_t* __restrict__ tail,
-                                           const uint8_t* __restrict__ row, BadTrack& bad,
-                                           const EvalItems& W) {
+                                           const uint8_t* __restrict__ row, const EvalItems& W) {
     const int J = I.J;
     const int END = J;
     const bool last = (Mnext == 0);
     const double* pcol = I.procT + (size_t)(I.stage_off[s] + (m < Ms ? m : 0)) * (J + 1);
-    double hr[NS], hp[NS];
+    double hr[NS];
     int hj[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-        int j = (work && m < Ms && k < Mprev) ? (int)nxt[J + 1 + k * G + m] : END;
+        const int j = (work && m < Ms && k < Mprev) ? (int)nxt[J + 1 + k * G + m] : END;
         hj[k] = j;
         hr[k] = ready[j];
-        hp[k] = __ldg(pcol + j);
     }
     uint16_t* mytail = tail + m * G;
     if (!last) {
 #pragma unroll
         for (int d = 0; d < G; ++d) mytail[d] = (uint16_t)(J + 1 + m * G + d);
     }
-    __syncwarp();
+    __syncthreads();
     if (work && m < Ms) {
         double avail = 0.0;
         while (true) {
-            int bs = 0;
-            double br = hr[0], bp = hp[0];
-            int bj = hj[0];
-#pragma unroll
-            for (int k = 1; k < NS; ++k) {
-                bool lt = (hr[k] < br) || (hr[k] == br && hj[k] < bj);
-                br = lt ? hr[k] : br;
-                bp = lt ? hp[k] : bp;
-                bj = lt ? hj[k] : bj;
-                bs = lt ? k : bs;
-            }
+            double br;
+            int bj;
+            head_min<NS>(hr, hj, br, bj);
             if (bj == END) break;
+            const double p = __ldg(pcol + bj);
             const int nh = nxt[bj];
             const double nr = ready[nh];
-            const double np = __ldg(pcol + nh);
             const double start = (br < avail) ? avail : br;  // std::max(ready, avail)
-            const double c = __dadd_rn(start, bp);
+            const double c = __dadd_rn(start, p);
             avail = c;
             ready[bj] = c;
             if (SCHED) {
@@ -111,41 +135,34 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 W.scomp[at] = c;
             }
             if (!last) {
-                const int d = row[bj];
-                if (d < Mnext) {
-                    const int t = mytail[d];
-                    nxt[t] = (uint16_t)bj;
-                    mytail[d] = (uint16_t)bj;
-                } else {
-                    bad.consider(c, bj);
-                }
+                const int d = min((int)row[bj], G - 1);
+                const int t = mytail[d];
+                nxt[t] = (uint16_t)bj;
+                mytail[d] = (uint16_t)bj;
             }
 #pragma unroll
-            for (int k = 0; k < NS; ++k)
-                if (k == bs) {
-                    hj[k] = nh;
-                    hr[k] = nr;
-                    hp[k] = np;
-                }
+            for (int k = 0; k < NS; ++k) {
+                const bool u = (hj[k] == bj);
+                hj[k] = u ? nh : hj[k];
+                hr[k] = u ? nr : hr[k];
+            }
         }
         if (!last) {
 #pragma unroll
             for (int d = 0; d < G; ++d) nxt[mytail[d]] = (uint16_t)END;
         }
     }
-    __syncwarp();
+    __syncthreads();
 }
 
 template <int G, bool SCHED>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                                int m, bool work, double* ready, uint16_t* nxt,
-                                               uint16_t* tail, const uint8_t* row, BadTrack& bad,
-                                               const EvalItems& W) {
+                                               uint16_t* tail, const uint8_t* row, const EvalItems& W) {
 #define FFSGA_STAGE(NS_)                                                                        \
     if constexpr (NS_ <= G) {                                                                    \
         if (Mprev <= NS_) {                                                                      \
-            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row,    \
-                                      bad, W);                                                   \
+            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, W); \
             return;                                                                              \
         }                                                                                        \
     }
@@ -162,16 +179,34 @@ __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mpre
 #undef FFSGA_STAGE
 }
 
+// Asynchronous copy of gene row s into `row` (cp.async, 16 B per request, L1 bypass).
 template <int G>
-__device__ __forceinline__ void load_row(const DevInst& I, const uint8_t* genes, int s, int m,
-                                         uint8_t* row) {
-    const uint4* src = reinterpret_cast<const uint4*>(genes + (size_t)s * I.Jpad);
-    uint4* dst = reinterpret_cast<uint4*>(row);
-    for (int v = m; v < I.Jpad / 16; v += G) dst[v] = __ldg(src + v);
+__device__ __forceinline__ void prefetch_row(const DevInst& I, const uint8_t* genes, int s, int m, uint8_t* row) {
+    const uint8_t* src = genes + (size_t)s * I.Jpad;
+    for (int v = m; v < I.Jpad / 16; v += G) __pipeline_memcpy_async(row + 16 * v, src + 16 * v, 16);
+    __pipeline_commit();
+}
+
+// Group-uniform: does the staged row hold a gene >= Mlimit (model.cpp:81-83)?  Every lane of
+// the warp must call it (the reduction shuffles).
+template <int G>
+__device__ __forceinline__ bool row_has_bad(const DevInst& I, const uint8_t* row, int m, int Mlimit, bool doit) {
+    unsigned bad = 0;
+    if (doit) {
+        const unsigned lim = 0x01010101u * (unsigned)min(Mlimit, 255);
+        const uint4* v4 = reinterpret_cast<const uint4*>(row);
+        for (int v = m; v < I.Jpad / 16; v += G) {
+            const uint4 x = v4[v];
+            bad |= __vcmpgeu4(x.x, lim) | __vcmpgeu4(x.y, lim) | __vcmpgeu4(x.z, lim) | __vcmpgeu4(x.w, lim);
+        }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) bad |= __shfl_xor_sync(kFull, bad, off, G);
+    return bad != 0;
 }
 
 template <int G, bool SCHED>
-__global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
+__global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int gw = lane / G;
@@ -181,37 +216,41 @@ __global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_
     double* ready = reinterpret_cast<double*>(gb);
     uint16_t* nxt = reinterpret_cast<uint16_t*>(gb + GL.off_next);
     uint16_t* tail = reinterpret_cast<uint16_t*>(gb + GL.off_tail);
-    uint8_t* row = gb + GL.off_row;
+    uint8_t* const row_a = gb + GL.off_row;
+    uint8_t* const row_b = gb + GL.off_row + I.Jpad;
     const int J = I.J, S = I.S;
     const int END = J;
     const long long n = W.n_dev ? *W.n_dev : W.n;
 
+    // all groups of the CTA share the item loop (CTA-uniform bounds: stage barriers)
     for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
          base += (long long)gridDim.x * groups_per_cta) {
         const long long item = base + gid;
         const bool active = item < n;
-        if (__all_sync(kFull, !active)) continue;
         const uint8_t* genes = nullptr;
         if (active) genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
 
-        // ---- init: ready = release, END sentinel = +inf; stage-0 gene row
+        // ---- init: ready = release, END sentinel = +inf; rows 0 and 1 in flight
         if (active) {
+            prefetch_row<G>(I, genes, 0, m, row_a);
+            if (S > 1) prefetch_row<G>(I, genes, 1, m, row_b);
             for (int j = m; j < J; j += G) ready[j] = __ldg(I.release + j);
             if (m == 0) ready[END] = dinf();
-            load_row<G>(I, genes, 0, m, row);
         }
         tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
+        __pipeline_wait_prior(S > 1 ? 1 : 0);
         __syncwarp();
 
         // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order.
         // A chunk of G consecutive release-order jobs is linked with one match_any per chunk.
+        const uint8_t* row0 = row_a;
         const int M0 = I.M[0];
         int bad_k = 0x7FFFFFFF;
         for (int b0 = 0; b0 < J; b0 += G) {
             const int k = b0 + m;
             const bool valid = active && k < J;
             const int j = valid ? (int)I.rel_order[k] : 0;
-            const int d = valid ? (int)row[j] : 0;
+            const int d = valid ? (int)row0[j] : 0;
             const bool good = valid && d < M0;
             if (valid && !good) bad_k = min(bad_k, k);
             const unsigned key = good ? (((unsigned)gw << 8) | (unsigned)d) : (0x10000u | (unsigned)lane);
@@ -233,25 +272,32 @@ __global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_
         if (active && bad_k != 0x7FFFFFFF) {
             work = false;
             if (m == 0 && W.err)
-                atomicMin(W.err, ((unsigned long long)item << 32) | (0ull << 16) |
-                                     (unsigned long long)I.rel_order[bad_k]);
+                atomicMin(W.err, ((unsigned long long)item << 32) | (unsigned long long)I.rel_order[bad_k]);
         }
-        __syncwarp();
 
         // ---- stages
         int Mprev = 1;
         for (int s = 0; s < S; ++s) {
             const int Ms = I.M[s];
             const int Mnext = (s + 1 < S) ? I.M[s + 1] : 0;
-            if (work && Mnext) load_row<G>(I, genes, s + 1, m, row);
-            BadTrack bad;
-            bad.reset();
-            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, bad, W);
-            if (Mnext) {
+            const uint8_t* row = ((s + 1) & 1) ? row_b : row_a;
+            __pipeline_wait_prior(0);  // row s+1 has landed
+            __syncwarp();
+            bool row_bad = false;
+            if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
+            if (work && s + 2 < S) prefetch_row<G>(I, genes, s + 2, m, (s & 1) ? row_b : row_a);
+            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, W);
+            if (__any_sync(kFull, row_bad)) {
+                // first offending job in stage s+1 dispatch order: min (ready, job) among them
+                BadTrack bad;
+                bad.reset();
+                if (row_bad)
+                    for (int j = m; j < J; j += G)
+                        if (row[j] >= Mnext) bad.consider(ready[j], j);
                 double bc = bad.c;
                 int bj = bad.j;
                 group_min_key<G>(bc, bj);
-                if (work && bj != 0x7FFFFFFF) {
+                if (row_bad && work && bj != 0x7FFFFFFF) {
                     work = false;
                     if (m == 0 && W.err)
                         atomicMin(W.err, ((unsigned long long)item << 32) |
@@ -260,6 +306,7 @@ __global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_
             }
             Mprev = Ms;
         }
+        __pipeline_wait_prior(0);
 
         // ---- report_from_completions (model.cpp:107-120)
         double mk = 0.0;
@@ -283,7 +330,7 @@ __global__ void __launch_bounds__(64) k_eval(DevInst I, EvalItems W, int groups_
             if (W.mk) W.mk[item] = mk;
             if (W.td) W.td[item] = T;
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -883,12 +930,12 @@ int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
     cfg->G = G;
     cfg->gl = group_layout(I.J, I.Jpad, G);
     const int max_smem = 227 * 1024;
-    int warps = 2;
-    if ((size_t)(32 * warps / G) * cfg->gl.bytes > (size_t)max_smem) warps = 1;
+    const size_t per_warp = (size_t)(32 / G) * cfg->gl.bytes;
+    int warps = (int)std::min<size_t>(16, max_smem / per_warp);
+    if (warps < 1) return -1;
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
     cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
-    if (cfg->smem > (size_t)max_smem) return -1;
     cudaError_t e = cudaFuncSetAttribute(k_eval<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
     if (e != cudaSuccess) return -2;
     e = cudaFuncSetAttribute(k_eval<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
