@@ -19,6 +19,8 @@ constexpr int kMaxMachines = 32;  // lanes per decoder group: one lane per machi
 struct DevInst {
     int J, S, Jpad, maxM;
     int bits_per_job, total_bits, words;
+    int cta_sync;   // decoder stage barriers: 1 = CTA-wide (shared procT slice in L1), 0 = per warp
+    int max_warps;  // decoder CTA size cap (0 = smem-limited, at most 16)
     double weight, emax;
     const int* M;               // [S]
     const int* stage_off;       // [S+1]
@@ -64,7 +66,7 @@ struct GroupLayout {
 __host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
 __host__ __device__ inline GroupLayout group_layout(int J, int Jpad, int G) {
     GroupLayout g;
-    int ready = align16(8 * (J + 1));                 // fp64 ready[J] + END sentinel (+inf)
+    int ready = align16(8 * (J + 1 + G * G));         // fp64 node values (jobs, END, dummies)
     int next = align16(2 * (J + 1 + G * G));          // u16 links + G*G list dummies
     int tail = align16(2 * G * G);                    // u16 tail[m][dst]
     g.off_next = ready;

@@ -57,114 +57,181 @@ __device__ __forceinline__ void group_min_key(double& c, int& j) {
 // Design: one group of G lanes per chromosome, lane m owns machine m of the
 // current stage; every group of a CTA advances stage by stage in lockstep (__syncthreads at
 // stage boundaries) so the CTA shares one stage slice of the processing-time table in L1.
-// Per-group shared memory: ready[J+1] fp64, link[J+1+G*G] u16, tail[G*G] u16, 2 gene rows.
+//
+// Per-group shared memory (node = job 0..J-1, END = J, list dummies J+1+src*G+dst):
+//   link[node] u16  -- next job of the node's list
+//   lval[node] fp64 -- ready time (previous-stage completion) of link[node]; +inf after END
+//   tail[G*G]  u16  -- tail node of each outgoing list of this stage
+//   two gene rows   -- stage s+1 (routing of this stage) and s+2 (cp.async prefetch)
+// Carrying the successor's ready time in the node lets a pop fetch both the next head and its
+// key with two independent loads.  After the last stage lval[j] holds job j's completion.
 
-// Lexicographic (ready, job) minimum of NS list heads by a fixed tournament (depth log2 NS),
-// predicated selects only.  Jobs are distinct, so the minimum is unique whatever the tree shape.
+__device__ __forceinline__ bool key_lt(double va, int ja, double vb, int jb) {  // (ready, job) order
+    return (va < vb) | ((va == vb) & (ja < jb));
+}
+
+// The NS list heads of a lane are kept sorted by (ready, job), so the next job to dispatch is
+// always head 0.  After a pop, the successor from the same list is inserted in one step: all
+// NS-1 comparisons are independent and each slot is rebuilt with two selects, so the
+// loop-carried dependency is one compare and two selects deep (not a log2(NS) tournament).
 template <int NS>
-__device__ __forceinline__ void head_min(const double (&hr)[NS], const int (&hj)[NS], double& br, int& bj) {
-    double r[NS];
-    int j[NS];
+__device__ __forceinline__ void heads_sort(double (&v)[NS], int (&j)[NS]) {
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        r[k] = hr[k];
-        j[k] = hj[k];
-    }
+    for (int i = 0; i < NS; ++i) {
 #pragma unroll
-    for (int stride = 1; stride < NS; stride *= 2) {
-#pragma unroll
-        for (int k = 0; k + stride < NS; k += 2 * stride) {
-            const bool lt = (r[k + stride] < r[k]) | ((r[k + stride] == r[k]) & (j[k + stride] < j[k]));
-            r[k] = lt ? r[k + stride] : r[k];
-            j[k] = lt ? j[k + stride] : j[k];
+        for (int k = NS - 1; k > i; --k) {
+            const bool sw = key_lt(v[k], j[k], v[k - 1], j[k - 1]);
+            const double v0 = v[k - 1], v1 = v[k];
+            const int j0 = j[k - 1], j1 = j[k];
+            v[k - 1] = sw ? v1 : v0;
+            v[k] = sw ? v0 : v1;
+            j[k - 1] = sw ? j1 : j0;
+            j[k] = sw ? j0 : j1;
         }
     }
-    br = r[0];
-    bj = j[0];
+}
+
+template <int NS>
+__device__ __forceinline__ void heads_replace_min(double (&v)[NS], int (&j)[NS], double x, int xj) {
+    bool c[NS];
+#pragma unroll
+    for (int k = 0; k + 1 < NS; ++k) c[k] = key_lt(v[k + 1], j[k + 1], x, xj);
+    double nv[NS];
+    int nj[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const bool after = (k + 1 < NS) ? c[k] : false;  // slot k takes head k+1
+        const bool here = (k == 0) ? true : c[k - 1];    // else slot k takes x if x belongs at k
+        const double keep = here ? x : v[k];
+        const int keepj = here ? xj : j[k];
+        nv[k] = after ? v[(k + 1 < NS) ? k + 1 : k] : keep;
+        nj[k] = after ? j[(k + 1 < NS) ? k + 1 : k] : keepj;
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        v[k] = nv[k];
+        j[k] = nj[k];
+    }
 }
 
 // One stage of the list schedule for the group's chromosome (model.cpp:68-95).
-// Lane m (< Ms) merges the NS incoming per-source linked lists of jobs routed to machine m
-// (each list is sorted by completion because completions on one machine strictly increase),
-// which reproduces the (ready, job) sort of model.cpp:72-75 restricted to machine m, then runs
-// the machine's fp64 recurrence start = max(ready, avail), completion = start + p (84-87).
-// Each dispatched job is appended to the outgoing list (m -> gene of the next stage).  The
-// loop body is branch-free: out-of-range next-stage genes were flagged when the row arrived
-// and are resolved after the stage (they only ever land in lists nobody reads).
+// Lane m (< Ms) merges the NS incoming per-source lists of jobs routed to machine m (each list
+// is sorted by completion because completions on one machine strictly increase), which
+// reproduces the (ready, job) sort of model.cpp:72-75 restricted to machine m, then runs the
+// machine's fp64 recurrence start = max(ready, avail), completion = start + p (84-87) and
+// appends the job to its outgoing list (m -> gene of the next stage).  Branch-free body:
+// out-of-range next-stage genes land in lists nobody reads and are reported after the stage.
+__device__ __forceinline__ void stage_barrier(bool cta) {
+    if (cta)
+        __syncthreads();
+    else
+        __syncwarp();
+}
+
 template <int G, int NS, bool SCHED>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
-                                           int m, bool work, double* __restrict__ ready,
-                                           uint16_t* __restrict__ nxt, uint16_t* __restrict__ tail,
-                                           const uint8_t* __restrict__ row, const EvalItems& W) {
+                                           int m, bool work, double* __restrict__ lval,
+                                           uint16_t* __restrict__ link, uint16_t* __restrict__ tail,
+                                           const uint8_t* __restrict__ row, bool check, BadTrack& bad,
+                                           const EvalItems& W) {
     const int J = I.J;
     const int END = J;
     const bool last = (Mnext == 0);
     const double* pcol = I.procT + (size_t)(I.stage_off[s] + (m < Ms ? m : 0)) * (J + 1);
-    double hr[NS];
+    double hv[NS];
     int hj[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-        const int j = (work && m < Ms && k < Mprev) ? (int)nxt[J + 1 + k * G + m] : END;
-        hj[k] = j;
-        hr[k] = ready[j];
+        const bool live = work && m < Ms && k < Mprev;
+        const int node = J + 1 + k * G + m;
+        hj[k] = live ? (int)link[node] : END;
+        hv[k] = live ? lval[node] : dinf();
     }
+    heads_sort<NS>(hv, hj);
     uint16_t* mytail = tail + m * G;
     if (!last) {
 #pragma unroll
         for (int d = 0; d < G; ++d) mytail[d] = (uint16_t)(J + 1 + m * G + d);
     }
-    __syncthreads();
+    stage_barrier(I.cta_sync);
     if (work && m < Ms) {
+        // Software pipelined by one pop: the processing-time load of pop i is consumed in
+        // iteration i+1, so its latency overlaps the next pop's list loads and head insertion.
+        // The delayed store lval[t_i] = c_i cannot alias iteration i+1's loads: t_i was
+        // dispatched already, the next head has not been.
         double avail = 0.0;
+        double q_br = 0.0, q_p = 0.0;  // pending pop: ready time and processing time
+        int q_j = END, q_t = 0, q_g = 0;
         while (true) {
-            double br;
-            int bj;
-            head_min<NS>(hr, hj, br, bj);
+            const int bj = hj[0];
             if (bj == END) break;
+            const double br = hv[0];
             const double p = __ldg(pcol + bj);
-            const int nh = nxt[bj];
-            const double nr = ready[nh];
-            const double start = (br < avail) ? avail : br;  // std::max(ready, avail)
-            const double c = __dadd_rn(start, p);
-            avail = c;
-            ready[bj] = c;
+            const int nh = link[bj];
+            const double nr = lval[bj];
+            const int g = last ? 0 : (int)row[bj];
+            heads_replace_min<NS>(hv, hj, nr, nh);
+            if (q_j != END) {  // retire the previous pop
+                const double start = (q_br < avail) ? avail : q_br;  // std::max(ready, avail)
+                const double c = __dadd_rn(start, q_p);
+                avail = c;
+                lval[q_t] = c;  // successor value of the list tail, or the final completion
+                if (SCHED) {
+                    const int at = q_j * I.S + s;
+                    W.smachine[at] = m;
+                    W.sstart[at] = start;
+                    W.scomp[at] = c;
+                }
+                if (check && q_g >= Mnext) bad.consider(c, q_j);
+            }
+            int t = bj;  // last stage: the completion goes to the job's own node
+            if (!last) {
+                const int d = min(g, G - 1);
+                t = mytail[d];
+                link[t] = (uint16_t)bj;
+                mytail[d] = (uint16_t)bj;
+            }
+            q_j = bj;
+            q_br = br;
+            q_p = p;
+            q_t = t;
+            q_g = g;
+        }
+        if (q_j != END) {
+            const double start = (q_br < avail) ? avail : q_br;
+            const double c = __dadd_rn(start, q_p);
+            lval[q_t] = c;
             if (SCHED) {
-                const int at = bj * I.S + s;
+                const int at = q_j * I.S + s;
                 W.smachine[at] = m;
                 W.sstart[at] = start;
                 W.scomp[at] = c;
             }
-            if (!last) {
-                const int d = min((int)row[bj], G - 1);
-                const int t = mytail[d];
-                nxt[t] = (uint16_t)bj;
-                mytail[d] = (uint16_t)bj;
-            }
-#pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                const bool u = (hj[k] == bj);
-                hj[k] = u ? nh : hj[k];
-                hr[k] = u ? nr : hr[k];
-            }
+            if (check && q_g >= Mnext) bad.consider(c, q_j);
         }
         if (!last) {
 #pragma unroll
-            for (int d = 0; d < G; ++d) nxt[mytail[d]] = (uint16_t)END;
+            for (int d = 0; d < G; ++d) {
+                const int t = mytail[d];
+                link[t] = (uint16_t)END;
+                lval[t] = dinf();
+            }
         }
     }
-    __syncthreads();
+    stage_barrier(I.cta_sync);
 }
 
 template <int G, bool SCHED>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
-                                               int m, bool work, double* ready, uint16_t* nxt,
-                                               uint16_t* tail, const uint8_t* row, const EvalItems& W) {
-#define FFSGA_STAGE(NS_)                                                                        \
-    if constexpr (NS_ <= G) {                                                                    \
-        if (Mprev <= NS_) {                                                                      \
-            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, W); \
-            return;                                                                              \
-        }                                                                                        \
+                                               int m, bool work, double* lval, uint16_t* link,
+                                               uint16_t* tail, const uint8_t* row, bool check, BadTrack& bad,
+                                               const EvalItems& W) {
+#define FFSGA_STAGE(NS_)                                                                              \
+    if constexpr (NS_ <= G) {                                                                          \
+        if (Mprev <= NS_) {                                                                            \
+            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, check, bad, W); \
+            return;                                                                                    \
+        }                                                                                              \
     }
     FFSGA_STAGE(1)
     FFSGA_STAGE(2)
@@ -213,8 +280,8 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
     const int m = lane % G;
     const int gid = threadIdx.x / G;
     unsigned char* gb = smem + (size_t)gid * GL.bytes;
-    double* ready = reinterpret_cast<double*>(gb);
-    uint16_t* nxt = reinterpret_cast<uint16_t*>(gb + GL.off_next);
+    double* lval = reinterpret_cast<double*>(gb);
+    uint16_t* link = reinterpret_cast<uint16_t*>(gb + GL.off_next);
     uint16_t* tail = reinterpret_cast<uint16_t*>(gb + GL.off_tail);
     uint8_t* const row_a = gb + GL.off_row;
     uint8_t* const row_b = gb + GL.off_row + I.Jpad;
@@ -228,31 +295,27 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         const long long item = base + gid;
         const bool active = item < n;
         const uint8_t* genes = nullptr;
-        if (active) genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
-
-        // ---- init: ready = release, END sentinel = +inf; rows 0 and 1 in flight
         if (active) {
+            genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
             prefetch_row<G>(I, genes, 0, m, row_a);
             if (S > 1) prefetch_row<G>(I, genes, 1, m, row_b);
-            for (int j = m; j < J; j += G) ready[j] = __ldg(I.release + j);
-            if (m == 0) ready[END] = dinf();
         }
         tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
         __pipeline_wait_prior(S > 1 ? 1 : 0);
         __syncwarp();
 
-        // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order.
-        // A chunk of G consecutive release-order jobs is linked with one match_any per chunk.
-        const uint8_t* row0 = row_a;
+        // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order;
+        // node values are release times.  G consecutive jobs are linked per match_any.
         const int M0 = I.M[0];
         int bad_k = 0x7FFFFFFF;
         for (int b0 = 0; b0 < J; b0 += G) {
             const int k = b0 + m;
             const bool valid = active && k < J;
             const int j = valid ? (int)I.rel_order[k] : 0;
-            const int d = valid ? (int)row0[j] : 0;
+            const int d = valid ? (int)row_a[j] : 0;
             const bool good = valid && d < M0;
             if (valid && !good) bad_k = min(bad_k, k);
+            const double rel = valid ? __ldg(I.release + j) : 0.0;
             const unsigned key = good ? (((unsigned)gw << 8) | (unsigned)d) : (0x10000u | (unsigned)lane);
             const unsigned peers = __match_any_sync(kFull, key);
             const unsigned below = peers & ((1u << lane) - 1u);
@@ -262,11 +325,19 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             int t = 0;
             if (good && !below) t = tail[d];
             __syncwarp();
-            if (good) nxt[below ? pred_j : t] = (uint16_t)j;
+            if (good) {
+                const int node = below ? pred_j : t;
+                link[node] = (uint16_t)j;
+                lval[node] = rel;
+            }
             if (good && !above) tail[d] = (uint16_t)j;
             __syncwarp();
         }
-        if (active) nxt[tail[m]] = (uint16_t)END;
+        if (active) {
+            const int t = tail[m];
+            link[t] = (uint16_t)END;
+            lval[t] = dinf();
+        }
         bad_k = group_min_int<G>(bad_k);
         bool work = active;
         if (active && bad_k != 0x7FFFFFFF) {
@@ -286,14 +357,11 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             bool row_bad = false;
             if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
             if (work && s + 2 < S) prefetch_row<G>(I, genes, s + 2, m, (s & 1) ? row_b : row_a);
-            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, ready, nxt, tail, row, W);
+            BadTrack bad;
+            bad.reset();
+            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, row_bad, bad, W);
             if (__any_sync(kFull, row_bad)) {
                 // first offending job in stage s+1 dispatch order: min (ready, job) among them
-                BadTrack bad;
-                bad.reset();
-                if (row_bad)
-                    for (int j = m; j < J; j += G)
-                        if (row[j] >= Mnext) bad.consider(ready[j], j);
                 double bc = bad.c;
                 int bj = bad.j;
                 group_min_key<G>(bc, bj);
@@ -308,21 +376,21 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         }
         __pipeline_wait_prior(0);
 
-        // ---- report_from_completions (model.cpp:107-120)
+        // ---- report_from_completions (model.cpp:107-120); completions are in lval[0..J)
         double mk = 0.0;
         if (work) {
             for (int j = m; j < J; j += G) {
-                const double c = ready[j];
+                const double c = lval[j];
                 mk = (mk < c) ? c : mk;
                 const double t = __dsub_rn(c, __ldg(I.due + j));
-                ready[j] = (0.0 < t) ? t : 0.0;  // std::max(0.0, c - due)
+                lval[j] = (0.0 < t) ? t : 0.0;  // std::max(0.0, c - due)
             }
         }
         mk = group_max<G>(mk);
         __syncwarp();
         if (work && m == 0) {
             double T = 0.0;  // sequential in job order: the fp64 sum is order dependent
-            for (int j = 0; j < J; ++j) T = __dadd_rn(T, ready[j]);
+            for (int j = 0; j < J; ++j) T = __dadd_rn(T, lval[j]);
             const double obj = __dadd_rn(__dmul_rn(I.weight, T), mk);
             const double f = __dsub_rn(I.emax, obj);
             W.obj[item] = obj;
@@ -330,7 +398,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             if (W.mk) W.mk[item] = mk;
             if (W.td) W.td[item] = T;
         }
-        __syncthreads();
+        stage_barrier(I.cta_sync);
     }
 }
 
@@ -931,7 +999,7 @@ int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
     cfg->gl = group_layout(I.J, I.Jpad, G);
     const int max_smem = 227 * 1024;
     const size_t per_warp = (size_t)(32 / G) * cfg->gl.bytes;
-    int warps = (int)std::min<size_t>(16, max_smem / per_warp);
+    int warps = (int)std::min<size_t>(I.max_warps > 0 ? I.max_warps : 16, max_smem / per_warp);
     if (warps < 1) return -1;
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
