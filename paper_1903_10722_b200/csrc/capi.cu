@@ -404,9 +404,9 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         d.release = I->dRelease.as<double>();
         d.due = I->dDue.as<double>();
         d.rel_order = I->dRelOrder.as<uint16_t>();
-        d.cta_sync = 1;
+        d.cta_sync = 0;  // per-warp stage barriers (measured best with the single staged row)
         d.max_warps = 0;
-        if (const char* v = std::getenv("FFSGA_EVAL_SYNC")) d.cta_sync = std::string(v) == "warp" ? 0 : 1;
+        if (const char* v = std::getenv("FFSGA_EVAL_SYNC")) d.cta_sync = std::string(v) == "cta" ? 1 : 0;
         if (const char* v = std::getenv("FFSGA_EVAL_WARPS")) d.max_warps = std::atoi(v);
         const int rc = eval_config(d, I->sm_count, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");

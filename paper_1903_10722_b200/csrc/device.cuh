@@ -72,7 +72,7 @@ __host__ __device__ inline GroupLayout group_layout(int J, int Jpad, int G) {
     g.off_next = ready;
     g.off_tail = ready + next;
     g.off_row = ready + next + tail;
-    g.bytes = g.off_row + 2 * Jpad;                   // u8 gene rows (next stage + prefetch)
+    g.bytes = g.off_row + Jpad;                       // u8 gene row of the next stage
     return g;
 }
 

@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
     uint16_t* link = reinterpret_cast<uint16_t*>(gb + GL.off_next);
     uint16_t* tail = reinterpret_cast<uint16_t*>(gb + GL.off_tail);
     uint8_t* const row_a = gb + GL.off_row;
-    uint8_t* const row_b = gb + GL.off_row + I.Jpad;
     const int J = I.J, S = I.S;
     const int END = J;
     const long long n = W.n_dev ? *W.n_dev : W.n;
@@ -298,10 +297,9 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         if (active) {
             genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
             prefetch_row<G>(I, genes, 0, m, row_a);
-            if (S > 1) prefetch_row<G>(I, genes, 1, m, row_b);
         }
         tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
-        __pipeline_wait_prior(S > 1 ? 1 : 0);
+        __pipeline_wait_prior(0);
         __syncwarp();
 
         // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order;
@@ -351,12 +349,16 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         for (int s = 0; s < S; ++s) {
             const int Ms = I.M[s];
             const int Mnext = (s + 1 < S) ? I.M[s + 1] : 0;
-            const uint8_t* row = ((s + 1) & 1) ? row_b : row_a;
+            const uint8_t* row = row_a;
+            __syncwarp();  // every lane is done with row s
+            if (work && s + 1 < S) prefetch_row<G>(I, genes, s + 1, m, row_a);
+            if (work && s + 2 < S)  // warm L2 with row s+2 (no shared memory spent on it)
+                for (int v = m; v * 128 < I.Jpad; v += G)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(genes + (size_t)(s + 2) * I.Jpad + v * 128));
             __pipeline_wait_prior(0);  // row s+1 has landed
             __syncwarp();
             bool row_bad = false;
             if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
-            if (work && s + 2 < S) prefetch_row<G>(I, genes, s + 2, m, (s & 1) ? row_b : row_a);
             BadTrack bad;
             bad.reset();
             dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, row_bad, bad, W);
