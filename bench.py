@@ -251,12 +251,18 @@ def main():
 
     import torch
     comm = None
+    if os.environ.get("FFSGA_BENCH_DEVICE") is not None:  # test hook: all ranks on one GPU
+        local = int(os.environ["FFSGA_BENCH_DEVICE"])
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FFSGA_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         from paper_1903_10722_b200.islands import TorchComm
-        comm = TorchComm(device=f"cuda:{local}")
+        comm = TorchComm(device=f"cuda:{local}" if backend == "nccl" else "cpu")
 
     from paper_1903_10722_b200 import capi
     from paper_1903_10722_b200.islands import IslandConfig, IslandModel

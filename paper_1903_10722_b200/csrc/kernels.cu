@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(256) k_unpack_rows(DevInst I, const unsigned l
 }
 
 // ---------------------------------------------------------------------------- K3 cellular breed
-constexpr int kMutChunk = 8;  // draws per lane per window of the mutation stream parse
+constexpr int kMutChunk = 16;  // draws per lane per window of the mutation stream parse
 
 // compute_cell (cellular.cpp:116-150) for one cell per warp.  The serial prefix (tournaments,
 // crossover coin and cut points) is replayed redundantly by every lane; the mutation loop
@@ -638,7 +638,7 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
     const unsigned long long thr = C.thr_mu;
     unsigned long long pos = k;
     unsigned long long end = k;
-    long long coins_before = 0;
+    int coins_before = 0;
     bool st_coin = true;
     while (coins_before < L || (coins_before == L && !st_coin)) {
         unsigned long long u[kMutChunk];
@@ -675,8 +675,7 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
         // exclusive prefix for this lane given the window entry state
         const int eF0 = __shfl_up_sync(kFull, F0, 1), eF1 = __shfl_up_sync(kFull, F1, 1);
         const int eC0 = __shfl_up_sync(kFull, C0, 1), eC1 = __shfl_up_sync(kFull, C1, 1);
-        int st;
-        long long g;
+        int st, g;
         if (lane == 0) {
             st = st_coin;
             g = coins_before;
@@ -684,23 +683,26 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
             st = st_coin ? eF1 : eF0;
             g = coins_before + (st_coin ? eC1 : eC0);
         }
-        // walk the slice: a coin for gene g, or the index draw of gene g-1 after a true coin
+        // (job, stage) of gene g and of gene g-1 (the owner of a leading index draw); advanced
+        // incrementally in the walk, one 32-bit division per lane and window
+        int cj = g / I.S, cs = g - cj * I.S;
+        int pj = cs == 0 ? cj - 1 : cj, ps = cs == 0 ? I.S - 1 : cs - 1;
+        // walk the slice: a coin for gene g, or the index draw of gene g-1 after a true coin.
+        // Branch-free (lanes disagree on which draws are coins): selects + a predicated store.
 #pragma unroll
         for (int t = 0; t < kMutChunk; ++t) {
-            if (st) {
-                const int bit = (tb >> t) & 1;
-                if (g == L - 1) end = p0 + t + 1 + (unsigned long long)bit;
-                ++g;
-                st = !bit;
-            } else {
-                const long long gene = g - 1;
-                if (gene < L) {
-                    const int s = (int)(gene % I.S);
-                    const int j = (int)(gene / I.S);
-                    child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(u[t], I.M[s]);
-                }
-                st = 1;
-            }
+            const bool bit = (tb >> t) & 1u;
+            const bool coin = st != 0;
+            end = (coin && g == L - 1) ? p0 + t + 1 + (bit ? 1ull : 0ull) : end;
+            const int v = index_of(u[t], __ldg(I.M + ps));
+            if (!coin && g - 1 < L) child[(size_t)ps * I.Jpad + pj] = (uint8_t)v;
+            const bool wrap = cs + 1 == I.S;
+            pj = coin ? cj : pj;
+            ps = coin ? cs : ps;
+            cj = (coin && wrap) ? cj + 1 : cj;
+            cs = coin ? (wrap ? 0 : cs + 1) : cs;
+            g += coin ? 1 : 0;
+            st = coin ? !bit : 1;
         }
         const int lF0 = __shfl_sync(kFull, F0, 31), lF1 = __shfl_sync(kFull, F1, 31);
         const int lC0 = __shfl_sync(kFull, C0, 31), lC1 = __shfl_sync(kFull, C1, 31);
