@@ -404,9 +404,11 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         d.release = I->dRelease.as<double>();
         d.due = I->dDue.as<double>();
         d.rel_order = I->dRelOrder.as<uint16_t>();
-        d.cta_sync = 0;  // per-warp stage barriers (measured best with the single staged row)
+        // CTA-wide stage barriers keep one stage slice of procT hot in L1 for the whole CTA; they
+        // pay off when the table does not fit L1 anyway (measured: 500x20 +14 %, 100x10 -11 %)
+        d.cta_sync = (size_t)MT * (J + 1) * sizeof(double) > (size_t)128 * 1024 ? 1 : 0;
         d.max_warps = 0;
-        if (const char* v = std::getenv("FFSGA_EVAL_SYNC")) d.cta_sync = std::string(v) == "cta" ? 1 : 0;
+        if (const char* v = std::getenv("FFSGA_EVAL_SYNC")) d.cta_sync = std::string(v) == "cta" ? 1 : (std::string(v) == "warp" ? 0 : d.cta_sync);
         if (const char* v = std::getenv("FFSGA_EVAL_WARPS")) d.max_warps = std::atoi(v);
         const int rc = eval_config(d, I->sm_count, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");

@@ -155,60 +155,48 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     }
     stage_barrier(I.cta_sync);
     if (work && m < Ms) {
-        // Software pipelined by one pop: the processing-time load of pop i is consumed in
-        // iteration i+1, so its latency overlaps the next pop's list loads and head insertion.
-        // The delayed store lval[t_i] = c_i cannot alias iteration i+1's loads: t_i was
-        // dispatched already, the next head has not been.
+        // Software pipelined by one pop: pop i is retired (recurrence, list append, stores) at
+        // the top of iteration i+1, so its processing-time and gene-row loads have a whole head
+        // insertion to arrive, and retiring before the next loads lets each pending value
+        // reuse its register (no copy that would wait on the load).  The deferred stores cannot
+        // alias iteration i+1's loads: they touch dispatched jobs or list dummies only.
         double avail = 0.0;
         double q_br = 0.0, q_p = 0.0;  // pending pop: ready time and processing time
-        int q_j = END, q_t = 0, q_g = 0;
-        while (true) {
-            const int bj = hj[0];
-            if (bj == END) break;
-            const double br = hv[0];
-            const double p = __ldg(pcol + bj);
-            const int nh = link[bj];
-            const double nr = lval[bj];
-            const int g = last ? 0 : (int)row[bj];
-            heads_replace_min<NS>(hv, hj, nr, nh);
-            if (q_j != END) {  // retire the previous pop
-                const double start = (q_br < avail) ? avail : q_br;  // std::max(ready, avail)
-                const double c = __dadd_rn(start, q_p);
-                avail = c;
-                lval[q_t] = c;  // successor value of the list tail, or the final completion
-                if (SCHED) {
-                    const int at = q_j * I.S + s;
-                    W.smachine[at] = m;
-                    W.sstart[at] = start;
-                    W.scomp[at] = c;
-                }
-                if (check && q_g >= Mnext) bad.consider(c, q_j);
-            }
-            int t = bj;  // last stage: the completion goes to the job's own node
-            if (!last) {
-                const int d = min(g, G - 1);
-                t = mytail[d];
-                link[t] = (uint16_t)bj;
-                mytail[d] = (uint16_t)bj;
-            }
-            q_j = bj;
-            q_br = br;
-            q_p = p;
-            q_t = t;
-            q_g = g;
-        }
-        if (q_j != END) {
-            const double start = (q_br < avail) ? avail : q_br;
+        int q_j = END, q_g = 0;
+        auto retire = [&]() {
+            const double start = (q_br < avail) ? avail : q_br;  // std::max(ready, avail)
             const double c = __dadd_rn(start, q_p);
-            lval[q_t] = c;
+            avail = c;
             if (SCHED) {
                 const int at = q_j * I.S + s;
                 W.smachine[at] = m;
                 W.sstart[at] = start;
                 W.scomp[at] = c;
             }
-            if (check && q_g >= Mnext) bad.consider(c, q_j);
+            if (!last) {
+                const int d = min(q_g, G - 1);
+                const int t = mytail[d];
+                link[t] = (uint16_t)q_j;
+                lval[t] = c;
+                mytail[d] = (uint16_t)q_j;
+                if (check && q_g >= Mnext) bad.consider(c, q_j);
+            } else {
+                lval[q_j] = c;  // final completion (the node was consumed by its pop)
+            }
+        };
+        while (true) {
+            const int bj = hj[0];
+            if (bj == END) break;
+            if (q_j != END) retire();
+            q_br = hv[0];
+            q_p = __ldg(pcol + bj);
+            q_g = last ? 0 : (int)row[bj];
+            q_j = bj;
+            const int nh = link[bj];
+            const double nr = lval[bj];
+            heads_replace_min<NS>(hv, hj, nr, nh);
         }
+        if (q_j != END) retire();
         if (!last) {
 #pragma unroll
             for (int d = 0; d < G; ++d) {
