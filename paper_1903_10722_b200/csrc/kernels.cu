@@ -128,15 +128,14 @@ __device__ __forceinline__ void stage_barrier(bool cta) {
         __syncwarp();
 }
 
-template <int G, int NS, bool SCHED>
+template <int G, int NS, bool SCHED, bool LAST>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                            int m, bool work, double* __restrict__ lval,
                                            uint16_t* __restrict__ link, uint16_t* __restrict__ tail,
-                                           const uint8_t* __restrict__ row, bool check, BadTrack& bad,
-                                           const EvalItems& W) {
+                                           const uint8_t* __restrict__ row, const EvalItems& W) {
     const int J = I.J;
     const int END = J;
-    const bool last = (Mnext == 0);
+    constexpr bool last = LAST;
     const double* pcol = I.procT + (size_t)(I.stage_off[s] + (m < Ms ? m : 0)) * (J + 1);
     double hv[NS];
     int hj[NS];
@@ -179,7 +178,6 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 link[t] = (uint16_t)q_j;
                 lval[t] = c;
                 mytail[d] = (uint16_t)q_j;
-                if (check && q_g >= Mnext) bad.consider(c, q_j);
             } else {
                 lval[q_j] = c;  // final completion (the node was consumed by its pop)
             }
@@ -212,14 +210,16 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
 template <int G, bool SCHED>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                                int m, bool work, double* lval, uint16_t* link,
-                                               uint16_t* tail, const uint8_t* row, bool check, BadTrack& bad,
-                                               const EvalItems& W) {
-#define FFSGA_STAGE(NS_)                                                                              \
-    if constexpr (NS_ <= G) {                                                                          \
-        if (Mprev <= NS_) {                                                                            \
-            stage_pass<G, NS_, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, check, bad, W); \
-            return;                                                                                    \
-        }                                                                                              \
+                                               uint16_t* tail, const uint8_t* row, const EvalItems& W) {
+#define FFSGA_STAGE(NS_)                                                                           \
+    if constexpr (NS_ <= G) {                                                                       \
+        if (Mprev <= NS_) {                                                                         \
+            if (Mnext)                                                                              \
+                stage_pass<G, NS_, SCHED, false>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W); \
+            else                                                                                    \
+                stage_pass<G, NS_, SCHED, true>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W);  \
+            return;                                                                                 \
+        }                                                                                           \
     }
     FFSGA_STAGE(1)
     FFSGA_STAGE(2)
@@ -232,6 +232,25 @@ __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mpre
     FFSGA_STAGE(16)
     FFSGA_STAGE(32)
 #undef FFSGA_STAGE
+}
+
+// Out-of-range genes of stage s+1 (rare): walk lane m's outgoing lists (their nodes carry each
+// job's stage-s completion) and return the first offender in stage s+1 dispatch order, i.e.
+// the minimum (completion, job) among jobs whose next-stage gene is >= Mnext.
+template <int G>
+__device__ __forceinline__ void find_bad(const DevInst& I, int m, int Ms, int Mnext, const double* lval,
+                                         const uint16_t* link, const uint8_t* row, BadTrack& bad) {
+    const int J = I.J;
+    if (m >= Ms) return;
+    for (int d = 0; d < G; ++d) {
+        int node = J + 1 + m * G + d;
+        while (true) {
+            const int j = link[node];
+            if (j == J) break;
+            if (row[j] >= Mnext) bad.consider(lval[node], j);
+            node = j;
+        }
+    }
 }
 
 // Asynchronous copy of gene row s into `row` (cp.async, 16 B per request, L1 bypass).
@@ -347,11 +366,12 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             __syncwarp();
             bool row_bad = false;
             if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
-            BadTrack bad;
-            bad.reset();
-            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, row_bad, bad, W);
+            dispatch_stage<G, SCHED>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W);
             if (__any_sync(kFull, row_bad)) {
                 // first offending job in stage s+1 dispatch order: min (ready, job) among them
+                BadTrack bad;
+                bad.reset();
+                if (row_bad && work) find_bad<G>(I, m, Ms, Mnext, lval, link, row, bad);
                 double bc = bad.c;
                 int bj = bad.j;
                 group_min_key<G>(bc, bj);
