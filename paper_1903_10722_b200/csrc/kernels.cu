@@ -187,7 +187,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             if (bj == END) break;
             if (q_j != END) retire();
             q_br = hv[0];
-            q_p = __ldg(pcol + bj);
+            q_p = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32 address
             q_g = last ? 0 : (int)row[bj];
             q_j = bj;
             const int nh = link[bj];
