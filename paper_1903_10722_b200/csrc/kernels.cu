@@ -522,28 +522,31 @@ __global__ void __launch_bounds__(256) k_pack_bits(DevInst I, const uint8_t* row
 }
 
 // bits_to_int (chromosome.cpp:44-59): slot value MSB-first, modulo the stage's machines.
-__device__ __forceinline__ unsigned extract_gene(const DevInst& I, const unsigned long long* wv, int j, int s) {
-    const int o = j * I.bits_per_job + I.sbo[s];
-    const int nb = I.bps[s];
+// bits_to_int (chromosome.cpp:44-59): slot value MSB-first, modulo the stage's machines.  The
+// slot holds bps = max(1, bit_width(M-1)) bits, so value < 2^bps < 2M and the modulo is a single
+// conditional subtraction.
+__device__ __forceinline__ unsigned extract_gene(const unsigned long long* wv, int o, int nb, unsigned M) {
     const int w = o >> 6, sh = o & 63;
     unsigned long long x = wv[w] >> sh;
     if (sh + nb > 64) x |= wv[w + 1] << (64 - sh);
     const unsigned raw = (unsigned)(x & ((1ull << nb) - 1ull));  // bit o at position 0
     const unsigned val = __brev(raw) >> (32 - nb);               // bit o becomes the MSB
-    return val % (unsigned)I.M[s];
+    return val >= M ? val - M : val;
 }
 
+// One job per lane: a job's slots are contiguous, and the 32 lanes of a warp write 32
+// consecutive bytes of each stage row.
 __device__ __forceinline__ void unpack_member(const DevInst& I, const unsigned long long* wv, uint8_t* dst,
                                               int lane) {
-    const int words_per_row = I.Jpad / 4;
-    for (int w = lane; w < I.S * words_per_row; w += 32) {
-        const int s = w / words_per_row;
-        const int j0 = (w % words_per_row) * 4;
-        unsigned v = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if (j0 + b < I.J) v |= extract_gene(I, wv, j0 + b, s) << (8 * b);
-        reinterpret_cast<unsigned*>(dst + (size_t)s * I.Jpad)[j0 / 4] = v;
+    for (int j = lane; j < I.Jpad; j += 32) {
+        if (j >= I.J) {
+            for (int s = 0; s < I.S; ++s) dst[(size_t)s * I.Jpad + j] = 0;
+            continue;
+        }
+        const int base = j * I.bits_per_job;
+        for (int s = 0; s < I.S; ++s)
+            dst[(size_t)s * I.Jpad + j] =
+                (uint8_t)extract_gene(wv, base + __ldg(I.sbo + s), __ldg(I.bps + s), (unsigned)__ldg(I.M + s));
     }
 }
 
