@@ -423,7 +423,12 @@ static int tournament(const int* slots, int n, const double* fitness, uint64_t* 
 }
 
 int orc_cellular_candidate(const orc_cellular* g, int index, uint64_t stream_seed,
-                           int* child, double* fit, double* obj) { /* :116-155 */
+                           int* child, double* fit, double* obj) {
+    return orc_cellular_candidate_draws(g, index, stream_seed, child, fit, obj, NULL);
+}
+
+int orc_cellular_candidate_draws(const orc_cellular* g, int index, uint64_t stream_seed,
+                                 int* child, double* fit, double* obj, uint64_t* draws) { /* :116-155 */
     const orc_instance* inst = g->inst;
     const int L = inst->num_jobs * inst->num_stages;
     const int n = g->neighbors_per_cell;
@@ -450,6 +455,11 @@ int orc_cellular_candidate(const orc_cellular* g, int index, uint64_t stream_see
     for (int i = 0; i < L; ++i)
         if (orc_rng_next_coin(&rng, g->mutation_rate))
             child[i] = orc_rng_next_index(&rng, inst->machines_per_stage[i % inst->num_stages]);
+    if (draws) {  /* state = seed + n * gamma (mod 2^64); gamma is odd, so n = delta * gamma^-1 */
+        uint64_t inv = GAMMA;
+        for (int it = 0; it < 6; ++it) inv *= 2 - GAMMA * inv;
+        *draws = (rng - stream_seed) * inv;
+    }
     orc_report rep;
     orc_score(inst, child, g->emax, &rep, NULL, NULL, NULL, NULL, NULL);
     if (rep.fitness > g->fitness[index]) {

@@ -117,6 +117,9 @@ void orc_cellular_free(orc_cellular* g);
  * child_genes, returns 1 if the child replaces the cell. */
 int orc_cellular_candidate(const orc_cellular* g, int index, uint64_t stream_seed,
                            int* child_genes, double* fit, double* obj);
+/* same, also returning the number of draws compute_cell consumed */
+int orc_cellular_candidate_draws(const orc_cellular* g, int index, uint64_t stream_seed,
+                                 int* child_genes, double* fit, double* obj, uint64_t* draws);
 void orc_cellular_step(orc_cellular* g); /* proj/src/cellular.cpp:164-182 */
 int orc_cellular_best_index(const orc_cellular* g); /* :184-189 */
 void orc_cellular_install(orc_cellular* g, int index, const int* genes, double fit, double obj);

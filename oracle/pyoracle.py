@@ -172,6 +172,8 @@ class Oracle:
         L.orc_cellular_free.argtypes = [_vp]
         L.orc_cellular_candidate.restype = _i32
         L.orc_cellular_candidate.argtypes = [_vp, _i32, _u64, _pi, _pd, _pd]
+        L.orc_cellular_candidate_draws.restype = _i32
+        L.orc_cellular_candidate_draws.argtypes = [_vp, _i32, _u64, _pi, _pd, _pd, _pu64]
         L.orc_cellular_step.argtypes = [_vp]
         L.orc_cellular_best_index.restype = _i32
         L.orc_cellular_best_index.argtypes = [_vp]
@@ -410,11 +412,13 @@ class OracleCellular:
     def best_index(self):
         return int(self.lib.orc_cellular_best_index(self.ptr))
 
-    def candidate(self, index, stream_seed):
+    def candidate(self, index, stream_seed, with_draws=False):
         child = np.empty(self.inst.data.num_genes, dtype=np.int32)
-        fit, obj = C.c_double(), C.c_double()
-        r = self.lib.orc_cellular_candidate(self.ptr, index, _u64(stream_seed), _ptr(child, _pi),
-                                            C.byref(fit), C.byref(obj))
+        fit, obj, dr = C.c_double(), C.c_double(), C.c_uint64()
+        r = self.lib.orc_cellular_candidate_draws(self.ptr, index, _u64(stream_seed), _ptr(child, _pi),
+                                                  C.byref(fit), C.byref(obj), C.byref(dr))
+        if with_draws:
+            return child, fit.value, obj.value, bool(r), dr.value
         return child, fit.value, obj.value, bool(r)
 
     def install(self, index, genes, fit, obj):

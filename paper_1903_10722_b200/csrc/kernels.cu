@@ -647,27 +647,32 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
 
     // mutation (cellular.cpp:148-150)
     const unsigned long long thr = C.thr_mu;
+    const bool always = thr >= (1ull << 53);                  // p = 1: every coin is true
+    const unsigned long long ulim = always ? 0ull : (thr << 11);  // (u>>11) < thr  <=>  u < thr<<11
     unsigned long long pos = k;
     unsigned long long end = k;
     int coins_before = 0;
     bool st_coin = true;
     while (coins_before < L || (coins_before == L && !st_coin)) {
-        unsigned long long u[kMutChunk];
-        unsigned tb = 0;
         const unsigned long long p0 = pos + (unsigned long long)lane * kMutChunk;
+        unsigned tb = 0;  // bit t: draw t would be a true coin
 #pragma unroll
         for (int t = 0; t < kMutChunk; ++t) {
-            u[t] = draw(cs, p0 + t);
-            tb |= (coin_of(u[t], thr) ? 1u : 0u) << t;
+            const unsigned long long u = draw(cs, p0 + t);
+            tb |= ((always || u < ulim) ? 1u : 0u) << t;
         }
-        // transfer function of this lane's slice for both entry states
-        int f1 = 1, c1 = 0, f0 = 0, c0 = 0;
+        // which draws of this lane's slice are coins, for both entry states
+        unsigned cm1 = 0, cm0 = 0;
+        int f1 = 1, f0 = 0;
 #pragma unroll
         for (int t = 0; t < kMutChunk; ++t) {
             const int bit = (tb >> t) & 1;
-            if (f1) { ++c1; f1 = !bit; } else { f1 = 1; }
-            if (f0) { ++c0; f0 = !bit; } else { f0 = 1; }
+            cm1 |= (unsigned)f1 << t;
+            cm0 |= (unsigned)f0 << t;
+            f1 = f1 ? !bit : 1;
+            f0 = f0 ? !bit : 1;
         }
+        const int c1 = __popc(cm1), c0 = __popc(cm0);
         // inclusive scan (composition) over lanes
         int F0 = f0, F1 = f1, C0 = c0, C1 = c1;
 #pragma unroll
@@ -694,26 +699,24 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
             st = st_coin ? eF1 : eF0;
             g = coins_before + (st_coin ? eC1 : eC0);
         }
-        // (job, stage) of gene g and of gene g-1 (the owner of a leading index draw); advanced
-        // incrementally in the walk, one 32-bit division per lane and window
-        int cj = g / I.S, cs = g - cj * I.S;
-        int pj = cs == 0 ? cj - 1 : cj, ps = cs == 0 ? I.S - 1 : cs - 1;
-        // walk the slice: a coin for gene g, or the index draw of gene g-1 after a true coin.
-        // Branch-free (lanes disagree on which draws are coins): selects + a predicated store.
-#pragma unroll
-        for (int t = 0; t < kMutChunk; ++t) {
-            const bool bit = (tb >> t) & 1u;
-            const bool coin = st != 0;
-            end = (coin && g == L - 1) ? p0 + t + 1 + (bit ? 1ull : 0ull) : end;
-            const int v = index_of(u[t], __ldg(I.M + ps));
-            if (!coin && g - 1 < L) child[(size_t)ps * I.Jpad + pj] = (uint8_t)v;
-            const bool wrap = cs + 1 == I.S;
-            pj = coin ? cj : pj;
-            ps = coin ? cs : ps;
-            cj = (coin && wrap) ? cj + 1 : cj;
-            cs = coin ? (wrap ? 0 : cs + 1) : cs;
-            g += coin ? 1 : 0;
-            st = coin ? !bit : 1;
+        const unsigned cm = st ? cm1 : cm0;  // coin draws of the slice: coin #r is gene g + r
+        // gene L-1's coin ends the loop's draws (plus its index draw when true)
+        const int ncoin = __popc(cm);
+        if (g <= L - 1 && L - 1 < g + ncoin) {
+            const int t = (int)__fns(cm, 0, L - g);  // (L-1-g)+1-th set bit
+            end = p0 + t + 1 + ((tb >> t) & 1u);
+        }
+        // index draws: right after a true coin (and draw 0 when the slice starts inside a pair)
+        unsigned im = ((cm & tb) << 1) & ((1u << kMutChunk) - 1u);
+        if (!st) im |= 1u;
+        while (im) {  // rare (mutation rate), divergent but short
+            const int t = __ffs(im) - 1;
+            im &= im - 1u;
+            const int gene = g + __popc(cm & ((1u << t) - 1u)) - 1;
+            if (gene < L) {
+                const int j = gene / I.S, s = gene - j * I.S;
+                child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(draw(cs, p0 + t), __ldg(I.M + s));
+            }
         }
         const int lF0 = __shfl_sync(kFull, F0, 31), lF1 = __shfl_sync(kFull, F1, 31);
         const int lC0 = __shfl_sync(kFull, C0, 31), lC1 = __shfl_sync(kFull, C1, 31);

@@ -143,7 +143,8 @@ def test_cell_candidate_matches_oracle(orc):
     for i in range(16):
         seed = orc.derive_seed(orc.derive_seed(123, 1), i)
         g, f, o, rep, used = dc.candidate(i, seed)
-        eg, ef, eo, erep = oc.candidate(i, seed)
+        eg, ef, eo, erep, edraws = oc.candidate(i, seed, with_draws=True)
+        assert used == edraws
         if not erep:  # cell_candidate returns the current cell when the child loses (cellular.cpp:157-162)
             eg = oc.genes()[i]
         assert np.array_equal(g, eg) and (f, o, rep) == (ef, eo, erep)
