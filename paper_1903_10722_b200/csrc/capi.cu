@@ -124,6 +124,8 @@ struct ffsga_cuda_instance_t {
     DevBuf dM, dStageOff, dBps, dSbo, dProcT, dRelease, dDue, dRelOrder, dBitStage;
     EvalConfig ec{};
     cudaStream_t stream = nullptr;
+    cudaStream_t stream2 = nullptr;  // pseudo islands of a joint step run beside the cellular ones
+    cudaEvent_t fork = nullptr, join = nullptr;
     std::mutex mu;
     // joint-step work list
     DevBuf wl_ptrs, wl_obj, wl_fit, wl_count, wl_scratch, cell_desc, pseudo_desc;
@@ -151,6 +153,9 @@ struct ffsga_cuda_instance_t {
     ~ffsga_cuda_instance_t() {
         cudaSetDevice(device);
         if (stream) cudaStreamDestroy(stream);
+        if (stream2) cudaStreamDestroy(stream2);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st0) cudaEventDestroy(st0);
@@ -174,14 +179,18 @@ struct ffsga_cuda_instance_t {
     // brackets a launch with events when timing is enabled (resolved by resolve_timing)
     template <typename F>
     void timed(int which, F&& f) {
+        timed_on(which, stream, f);
+    }
+    template <typename F>
+    void timed_on(int which, cudaStream_t st, F&& f) {
         if (!timing) {
             f();
             return;
         }
         Pending p{which, take_event(), take_event()};
-        CK(cudaEventRecord(p.a, stream));
+        CK(cudaEventRecord(p.a, st));
         f();
-        CK(cudaEventRecord(p.b, stream));
+        CK(cudaEventRecord(p.b, st));
         pending.push_back(p);
     }
     void resolve_timing() {
@@ -414,11 +423,14 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&I->stream2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&I->fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&I->join, cudaEventDisableTiming));
         CK(cudaEventCreate(&I->ev0));
         CK(cudaEventCreate(&I->ev1));
         CK(cudaEventCreate(&I->st0));
         CK(cudaEventCreate(&I->st1));
-        I->wl_count.alloc(sizeof(long long));
+        I->wl_count.alloc(2 * sizeof(long long));  // [0] cellular items, [1] crossed pseudo members
         I->eval_total.alloc(sizeof(unsigned long long));
         CK(cudaMemset(I->eval_total.p, 0, sizeof(unsigned long long)));
         *out = hold.release();
@@ -1228,28 +1240,52 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         I->pseudo_desc.ensure(sizeof(PseudoIsland) * std::max(1, np));
         if (nc) CK(cudaMemcpyAsync(I->cell_desc.p, cd.data(), sizeof(CellIsland) * nc, cudaMemcpyHostToDevice, I->stream));
         if (np) CK(cudaMemcpyAsync(I->pseudo_desc.p, pd.data(), sizeof(PseudoIsland) * np, cudaMemcpyHostToDevice, I->stream));
-        WorkList wl{};
-        wl.ptrs = I->wl_ptrs.as<const uint8_t*>();
-        wl.obj = I->wl_obj.as<double>();
-        wl.fit = I->wl_fit.as<double>();
-        wl.count = I->wl_count.as<long long>();
-        wl.scratch = I->wl_scratch.as<uint8_t>();
-        wl.scratch0 = n_cells;
-        wl.total = I->eval_total.as<unsigned long long>();
+        // Cellular and pseudo islands never read each other between rendezvous, so each kind
+        // runs its breed -> evaluate -> commit chain on its own stream and the GPU overlaps the
+        // integer-bound breeding of one with the latency-bound decoding of the other.
+        WorkList wc{}, wp{};
+        wc.ptrs = I->wl_ptrs.as<const uint8_t*>();
+        wc.obj = I->wl_obj.as<double>();
+        wc.fit = I->wl_fit.as<double>();
+        wc.count = I->wl_count.as<long long>();
+        wc.total = I->eval_total.as<unsigned long long>();
+        wp = wc;
+        wp.ptrs += n_cells;
+        wp.obj += n_cells;
+        wp.fit += n_cells;
+        wp.count = I->wl_count.as<long long>() + 1;
+        wp.scratch = I->wl_scratch.as<uint8_t>();
+        wp.scratch0 = 0;
         const CellIsland* cdev = I->cell_desc.as<CellIsland>();
         const PseudoIsland* pdev = I->pseudo_desc.as<PseudoIsland>();
-        EvalItems W{};
-        W.n_dev = wl.count;
-        W.ptrs = wl.ptrs;
-        W.obj = wl.obj;
-        W.fit = wl.fit;
+        EvalItems Wc{}, Wp{};
+        Wc.n = n_cells;
+        Wc.ptrs = wc.ptrs;
+        Wc.obj = wc.obj;
+        Wc.fit = wc.fit;
+        Wp.n_dev = wp.count;
+        Wp.ptrs = wp.ptrs;
+        Wp.obj = wp.obj;
+        Wp.fit = wp.fit;
+        CK(cudaEventRecord(I->fork, I->stream));
+        CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
         CK(cudaEventRecord(I->st0, I->stream));
         for (int g = 0; g < generations; ++g) {
-            I->timed(1, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, pdev, np, n_pairs, wl, I->stream)); });
-            I->timed(0, [&] { CK(launch_eval(I->d, I->ec, W, cap, I->sm_count, false, I->stream)); });
-            I->timed(2, [&] { CK(launch_commit(I->d, cdev, nc, pdev, np, wl, I->stream)); });
-            g_launches += 3 + (nc > 0 ? 1 : 0) + (np > 0 ? 1 : 0);
+            if (nc) {
+                I->timed_on(1, I->stream, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, nullptr, 0, 0, wc, I->stream)); });
+                I->timed_on(0, I->stream, [&] { CK(launch_eval(I->d, I->ec, Wc, n_cells, I->sm_count, false, I->stream)); });
+                I->timed_on(2, I->stream, [&] { CK(launch_commit(I->d, cdev, nc, nullptr, 0, wc, I->stream)); });
+                g_launches += 4;
+            }
+            if (np) {
+                I->timed_on(1, I->stream2, [&] { CK(launch_breed(I->d, nullptr, 0, 0, pdev, np, n_pairs, wp, I->stream2)); });
+                I->timed_on(0, I->stream2, [&] { CK(launch_eval(I->d, I->ec, Wp, 2 * n_pairs, I->sm_count, false, I->stream2)); });
+                I->timed_on(2, I->stream2, [&] { CK(launch_commit(I->d, nullptr, 0, pdev, np, wp, I->stream2)); });
+                g_launches += 4;
+            }
         }
+        CK(cudaEventRecord(I->join, I->stream2));
+        CK(cudaStreamWaitEvent(I->stream, I->join, 0));
         CK(cudaEventRecord(I->st1, I->stream));
         I->step_recorded = true;
         for (int i = 0; i < nc; ++i) {

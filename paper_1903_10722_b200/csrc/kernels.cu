@@ -1109,7 +1109,7 @@ cudaError_t launch_rows_to_int(const DevInst& I, const uint8_t* rows, long long 
 cudaError_t launch_breed(const DevInst& I, const CellIsland* cells_dev, int nc, long long n_cells,
                          const PseudoIsland* pseudo_dev, int np, long long n_pairs, const WorkList& wl,
                          cudaStream_t st) {
-    k_gen_begin<<<1, 1, 0, st>>>(wl.count, n_cells);
+    k_gen_begin<<<1, 1, 0, st>>>(wl.count, nc > 0 ? n_cells : 0);
     if (n_cells > 0) k_cell_breed<<<blocks_for(n_cells * 32, 256), 256, 0, st>>>(I, cells_dev, nc, n_cells, wl);
     if (n_pairs > 0) k_pseudo_breed<<<blocks_for(n_pairs * 32, 256), 256, 0, st>>>(I, pseudo_dev, np, n_pairs, wl);
     return cudaGetLastError();
