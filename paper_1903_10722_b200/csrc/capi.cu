@@ -805,8 +805,7 @@ int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, 
         c->npc = (int)(c->slots_host.size() / c->n);
         upload(c->slots, c->slots_host);
         const size_t block = I->block();
-        c->genes.alloc(2 * (size_t)c->n * block);
-        CK(cudaMemset(c->genes.p, 0, 2 * (size_t)c->n * block));
+        c->genes.alloc(2 * (size_t)c->n * block);  // slot 1 is written by the first breed, pads included
         c->sel.alloc(2 * (size_t)c->n);
         CK(cudaMemset(c->sel.p, 0, 2 * (size_t)c->n));
         c->fit.alloc(2 * sizeof(double) * c->n);

@@ -131,3 +131,28 @@ def test_against_compiled_reference(capi, orc, ref):
     eo, ef, em, et = ri.score_batch(pop, emax, workers=8)
     assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
     assert np.array_equal(mk, em) and np.array_equal(td, et)
+
+
+def test_full_size_sweep_properties(capi, orc):
+    """BASELINE C5 size (1M chromosomes, 500 x 20): a spread sample is bitwise equal to the oracle
+    and every result satisfies the size-independent invariants of report_from_completions."""
+    d = synthetic(orc, 500, 20)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    n = 1 << 20
+    b = capi.Batch(inst, n)
+    b.fill_random(99, 0, n)
+    b.evaluate(n)
+    obj, fit, mk, td = b.results(n, full=True)
+    slack = emax - obj
+    assert np.array_equal(fit, np.where(slack < 0.0, 0.0, slack))
+    assert np.all(mk > 0) and np.all(td >= 0) and np.all(np.isfinite(obj))
+    assert np.array_equal(obj, d.weight * td + mk)
+    idx = np.linspace(0, n - 1, 200).astype(np.int64)
+    for i in idx[::10]:
+        g = b.download(int(i), 1)[0]
+        r = oi.score(g, emax)
+        assert (r["objective"], r["fitness"], r["makespan"], r["total_tardiness"]) == (obj[i], fit[i], mk[i], td[i])
+    want = oi.random_population(99, 12345, 1)[0]
+    assert np.array_equal(b.download(12345, 1)[0], want)

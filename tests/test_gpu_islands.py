@@ -175,3 +175,21 @@ def test_install(capi, orc):
         dp.install(*args)
         op.install(*args)
         check_pseudo(dp, op)
+
+
+def test_c3_shape_islands_match_oracle(capi, orc):
+    """C3 instance shape (500 x 20, M in [2, 8]) on small islands, every member every generation."""
+    d = synthetic(orc, 500, 20)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    dc = capi.Cellular(inst, 16, 8, orc.derive_seed(1, 0))
+    dp = capi.Pseudo(inst, 64, orc.derive_seed(1, 1))
+    oc = oi.cellular(emax, 16, 8, orc.derive_seed(1, 0))
+    op = oi.pseudo(emax, 64, orc.derive_seed(1, 1))
+    for _ in range(3):
+        capi.step([dc], [dp], 1)
+        oc.step()
+        op.step()
+        check_cell(dc, oc)
+        check_pseudo(dp, op)
