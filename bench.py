@@ -312,6 +312,13 @@ def main():
             ms_max, evals_all = dev_ms, float(evals)
         gens_per_s = args.steps / (ms_max / 1e3)
         algo_bytes = evals * (L + 16)
+        traffic = None  # DRAM bytes per K1 launch from the committed ncu capture, scaled per evaluation
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+                tr = json.load(f)
+            traffic = tr["traffic_bytes_per_eval"] * (evals / max(1, eval_n))
+        except Exception:
+            pass
         achieved = algo_bytes / (eval_ms / 1e3) / 1e9 if eval_ms > 0 else 0.0
 
         # e2e: the public API call a user makes (instance upload, island init, K generations,
@@ -349,10 +356,13 @@ def main():
                 "evals_per_s": evals_all / (ms_max / 1e3),
                 "evals_per_step": evals_all / args.steps,
                 "kernel_ms_per_step": {"eval": eval_ms / args.steps, "breed": breed_ms / args.steps,
-                                       "commit": commit_ms / args.steps},
+                                       "commit": commit_ms / args.steps,
+                                       "note": "summed per stream; the cellular and pseudo chains overlap"},
                 "roofline": {"bound": "hbm", "kernel": "k_eval (K1 decoder)", "achieved": achieved,
                              "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                             "frac": achieved / hbm_peak, "traffic": None,
+                             "frac": achieved / hbm_peak, "traffic": traffic,
+                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1_traffic.json)",
+                             "algorithmic_bytes_per_launch": algo_bytes / max(1, eval_n),
                              "algorithmic_bytes_per_eval": L + 16,
                              "note": "decoder is latency/issue bound (fp64 max/add chains + smem list "
                                      "merges); see profiles/ for issue-active and DRAM counters"},
