@@ -126,6 +126,10 @@ struct ffsga_cuda_instance_t {
     cudaStream_t stream = nullptr;
     cudaStream_t stream2 = nullptr;  // pseudo islands of a joint step run beside the cellular ones
     cudaEvent_t fork = nullptr, join = nullptr;
+    // CUDA graph of `graph_chunk` generations of the last joint step (relaunched while the
+    // island set and the work-list buffers are unchanged)
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<const void*> graph_key;
     std::mutex mu;
     // joint-step work list
     DevBuf wl_ptrs, wl_obj, wl_fit, wl_count, wl_scratch, cell_desc, pseudo_desc;
@@ -156,6 +160,7 @@ struct ffsga_cuda_instance_t {
         if (stream2) cudaStreamDestroy(stream2);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (st0) cudaEventDestroy(st0);
@@ -1266,25 +1271,73 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         Wp.ptrs = wp.ptrs;
         Wp.obj = wp.obj;
         Wp.fit = wp.fit;
-        CK(cudaEventRecord(I->fork, I->stream));
-        CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
+        auto enqueue = [&](int gens, bool timed) {
+            CK(cudaEventRecord(I->fork, I->stream));
+            CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
+            for (int g = 0; g < gens; ++g) {
+                if (nc) {
+                    auto b = [&] { CK(launch_breed(I->d, cdev, nc, n_cells, nullptr, 0, 0, wc, I->stream)); };
+                    auto e = [&] { CK(launch_eval(I->d, I->ec, Wc, n_cells, I->sm_count, false, I->stream)); };
+                    auto c = [&] { CK(launch_commit(I->d, cdev, nc, nullptr, 0, wc, I->stream)); };
+                    if (timed) {
+                        I->timed_on(1, I->stream, b);
+                        I->timed_on(0, I->stream, e);
+                        I->timed_on(2, I->stream, c);
+                    } else {
+                        b();
+                        e();
+                        c();
+                    }
+                }
+                if (np) {
+                    auto b = [&] { CK(launch_breed(I->d, nullptr, 0, 0, pdev, np, n_pairs, wp, I->stream2)); };
+                    auto e = [&] { CK(launch_eval(I->d, I->ec, Wp, 2 * n_pairs, I->sm_count, false, I->stream2)); };
+                    auto c = [&] { CK(launch_commit(I->d, nullptr, 0, pdev, np, wp, I->stream2)); };
+                    if (timed) {
+                        I->timed_on(1, I->stream2, b);
+                        I->timed_on(0, I->stream2, e);
+                        I->timed_on(2, I->stream2, c);
+                    } else {
+                        b();
+                        e();
+                        c();
+                    }
+                }
+            }
+            CK(cudaEventRecord(I->join, I->stream2));
+            CK(cudaStreamWaitEvent(I->stream, I->join, 0));
+        };
+        const long long per_gen = (nc ? 4 : 0) + (np ? 4 : 0);
+        const bool use_graph = !I->timing && generations >= 2 && !std::getenv("FFSGA_NO_GRAPH");
         CK(cudaEventRecord(I->st0, I->stream));
-        for (int g = 0; g < generations; ++g) {
-            if (nc) {
-                I->timed_on(1, I->stream, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, nullptr, 0, 0, wc, I->stream)); });
-                I->timed_on(0, I->stream, [&] { CK(launch_eval(I->d, I->ec, Wc, n_cells, I->sm_count, false, I->stream)); });
-                I->timed_on(2, I->stream, [&] { CK(launch_commit(I->d, cdev, nc, nullptr, 0, wc, I->stream)); });
-                g_launches += 4;
+        if (use_graph) {
+            // the generation sequence is launch-bound for small islands: capture a chunk of
+            // generations once (device-side generation counters make it replayable)
+            const int chunk = std::min(generations, 16);
+            const std::vector<const void*> key = {cdev, pdev, wc.ptrs, wc.obj, wp.scratch, I->wl_count.p,
+                                                  (const void*)(intptr_t)nc, (const void*)(intptr_t)np,
+                                                  (const void*)(intptr_t)n_cells, (const void*)(intptr_t)n_pairs,
+                                                  (const void*)(intptr_t)chunk};
+            if (!I->graph_exec || I->graph_key != key) {
+                if (I->graph_exec) {
+                    CK(cudaGraphExecDestroy(I->graph_exec));
+                    I->graph_exec = nullptr;
+                }
+                cudaGraph_t graph = nullptr;
+                CK(cudaStreamBeginCapture(I->stream, cudaStreamCaptureModeThreadLocal));
+                enqueue(chunk, false);
+                CK(cudaStreamEndCapture(I->stream, &graph));
+                cudaError_t e = cudaGraphInstantiate(&I->graph_exec, graph, 0);
+                cudaGraphDestroy(graph);
+                CK(e);
+                I->graph_key = key;
             }
-            if (np) {
-                I->timed_on(1, I->stream2, [&] { CK(launch_breed(I->d, nullptr, 0, 0, pdev, np, n_pairs, wp, I->stream2)); });
-                I->timed_on(0, I->stream2, [&] { CK(launch_eval(I->d, I->ec, Wp, 2 * n_pairs, I->sm_count, false, I->stream2)); });
-                I->timed_on(2, I->stream2, [&] { CK(launch_commit(I->d, nullptr, 0, pdev, np, wp, I->stream2)); });
-                g_launches += 4;
-            }
+            for (int done = 0; done + chunk <= generations; done += chunk) CK(cudaGraphLaunch(I->graph_exec, I->stream));
+            if (generations % chunk) enqueue(generations % chunk, false);
+        } else {
+            enqueue(generations, true);
         }
-        CK(cudaEventRecord(I->join, I->stream2));
-        CK(cudaStreamWaitEvent(I->stream, I->join, 0));
+        g_launches += per_gen * generations;
         CK(cudaEventRecord(I->st1, I->stream));
         I->step_recorded = true;
         for (int i = 0; i < nc; ++i) {
