@@ -1038,15 +1038,15 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         p->trace.alloc(sizeof(double));
         // pairs (x, ~x): x = pair p's chromosome of the sequential init stream (pseudo.cpp:40-47)
         const size_t block = I->block();
-        DevBuf rows;
-        rows.alloc(block * (size_t)population);
-        CK(launch_random_rows(I->d, rows.as<uint8_t>(), (long long)block, population / 2, seed, 0, false, I->stream));
-        CK(launch_pack_bits(I->d, rows.as<uint8_t>(), (long long)block, nullptr, p->words.as<unsigned long long>(), nullptr,
+        I->wl_scratch.ensure(block * (size_t)population);  // shared scratch arena: no per-island malloc/free
+        uint8_t* rows = I->wl_scratch.as<uint8_t>();
+        CK(launch_random_rows(I->d, rows, (long long)block, population / 2, seed, 0, false, I->stream));
+        CK(launch_pack_bits(I->d, rows, (long long)block, nullptr, p->words.as<unsigned long long>(), nullptr,
                             population / 2, true, I->dBitStage.as<uint16_t>(), I->stream));
-        CK(launch_unpack_rows(I->d, p->words.as<unsigned long long>(), nullptr, rows.as<uint8_t>(), (long long)block, nullptr,
+        CK(launch_unpack_rows(I->d, p->words.as<unsigned long long>(), nullptr, rows, (long long)block, nullptr,
                               population, I->stream));
         g_launches += 3;
-        eval_rows(I, rows.as<uint8_t>(), population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, true);
+        eval_rows(I, rows, population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, true);
         const unsigned long long code = read_error(I);
         if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
         PseudoIsland& d = p->d;
@@ -1308,7 +1308,9 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             CK(cudaStreamWaitEvent(I->stream, I->join, 0));
         };
         const long long per_gen = (nc ? 4 : 0) + (np ? 4 : 0);
-        const bool use_graph = !I->timing && generations >= 2 && !std::getenv("FFSGA_NO_GRAPH");
+        // graphs pay off when a generation is launch bound (small islands); capturing costs
+        // ~0.1 s, so large work lists run plain launches
+        const bool use_graph = !I->timing && generations >= 2 && cap <= 16384 && !std::getenv("FFSGA_NO_GRAPH");
         CK(cudaEventRecord(I->st0, I->stream));
         if (use_graph) {
             // the generation sequence is launch-bound for small islands: capture a chunk of
