@@ -359,9 +359,9 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
                 fail(FFSGA_ERR_CONTRACT, "instance: release and due times must be finite");
         // completions on a machine must strictly increase for the merge-ordered decoder:
         // x + p > x for every completion x <= horizon iff p >= ulp(horizon)
+        // (instances violating it run on the bucket-sort decoder, which needs no such bound)
         const double ulp = std::nextafter(horizon, INFINITY) - horizon;
-        if (!(min_p >= ulp))
-            fail(FFSGA_ERR_CONFIG, "device decoder needs processing times >= ulp(schedule horizon)");
+        const bool merge_ok = min_p >= ulp;
         I->weight = weight;
         I->emax = emax;
         // stage-major proc columns with one zero pad per column
@@ -424,6 +424,16 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         d.max_warps = 0;
         if (const char* v = std::getenv("FFSGA_EVAL_SYNC")) d.cta_sync = std::string(v) == "cta" ? 1 : (std::string(v) == "warp" ? 0 : d.cta_sync);
         if (const char* v = std::getenv("FFSGA_EVAL_WARPS")) d.max_warps = std::atoi(v);
+        d.algo = merge_ok ? 0 : 1;
+        d.bshift = 0;
+        if (const char* v = std::getenv("FFSGA_EVAL_ALGO")) {
+            if (std::string(v) == "bucket") d.algo = 1;
+            if (std::string(v) == "merge") {
+                if (!merge_ok) fail(FFSGA_ERR_CONFIG, "merge decoder needs processing times >= ulp(schedule horizon)");
+                d.algo = 0;
+            }
+        }
+        if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
         const int rc = eval_config(d, I->sm_count, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));

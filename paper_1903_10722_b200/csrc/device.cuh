@@ -21,6 +21,8 @@ struct DevInst {
     int bits_per_job, total_bits, words;
     int cta_sync;   // decoder stage barriers: 1 = CTA-wide (shared procT slice in L1), 0 = per warp
     int max_warps;  // decoder CTA size cap (0 = smem-limited, at most 16)
+    int algo;       // decoder: 0 = k-way merge of per-source lists, 1 = per-stage bucket sort
+    int bshift;     // bucket decoder: J << bshift histogram buckets per stage
     double weight, emax;
     const int* M;               // [S]
     const int* stage_off;       // [S+1]
@@ -74,6 +76,25 @@ __host__ __device__ inline GroupLayout group_layout(int J, int Jpad, int G) {
     g.off_row = ready + next + tail;
     g.bytes = g.off_row + Jpad;                       // u8 gene row of the next stage
     return g;
+}
+
+struct BucketLayout {
+    int off_row, off_cnt, off_scat, off_fin, bytes, nb_cap, nbj;
+};
+// per group: keys fp64[J] | gene row u8[Jpad] | histogram u16[nb_cap] | scatter u16[J] | order u16[J]
+// nbj = histogram buckets per stage (J << bshift, or J >> -bshift), split evenly over the machines
+__host__ __device__ inline BucketLayout bucket_layout(int J, int Jpad, int G, int bshift) {
+    BucketLayout b;
+    b.nbj = bshift >= 0 ? (J << bshift) : (J >> -bshift);
+    if (b.nbj < 1) b.nbj = 1;
+    const int vec = 8 * G;  // u16 counters per lane-round of the vectorised scan
+    b.nb_cap = ((b.nbj + 32 + vec - 1) / vec) * vec;
+    b.off_row = align16(8 * J);
+    b.off_cnt = b.off_row + align16(Jpad);
+    b.off_scat = b.off_cnt + 2 * b.nb_cap;
+    b.off_fin = b.off_scat + align16(2 * J);
+    b.bytes = b.off_fin + align16(2 * J);
+    return b;
 }
 
 struct BadTrack {  // first out-of-range gene in the next stage's dispatch order: min (ready, job)

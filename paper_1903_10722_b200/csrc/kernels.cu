@@ -15,6 +15,7 @@
 #include <cuda_pipeline.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "launch.h"
 
@@ -405,6 +406,294 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             const double f = __dsub_rn(I.emax, obj);
             W.obj[item] = obj;
             W.fit[item] = (f < 0.0) ? 0.0 : f;  // std::max(emax - obj, 0.0)
+            if (W.mk) W.mk[item] = mk;
+            if (W.td) W.td[item] = T;
+        }
+        stage_barrier(I.cta_sync);
+    }
+}
+
+
+// ---------------------------------------------------------------------------- K1b bucket decoder
+// Alternative K1 (FFSGA_EVAL_ALGO=bucket): the per-stage (ready, job) order of model.cpp:72-75,
+// restricted to each machine, is built by a counting sort instead of a k-way merge, so only the
+// machine recurrence stays serial.  Per stage, all G lanes of the group work on all J jobs:
+//   P1  bucket = (machine, floor((ready - lo) * NBd / (hi - lo))) -> u16 histogram (smem atomics);
+//       the map ready -> bucket is monotone (RN sub/mul and truncation never invert an order),
+//       so buckets are ordered like their keys and only jobs inside one bucket need comparing;
+//   P2  exclusive scan of the histogram (bucket start offsets);
+//   P3  scatter jobs to their bucket (atomic cursor; order inside a bucket arbitrary);
+//   P4  exact rank inside the bucket by (ready, job) -> final per-machine dispatch order;
+//   P5  lane m runs machine m's recurrence start = max(ready, avail), C = start + p
+//       (model.cpp:84-87) over its jobs in order, writing C in place of ready.
+// Stage 0 sorts by the release rank (distinct integers; model.cpp:98-105) and reads the release
+// times in P5.  lo/hi of the next stage are the first/last completion of each machine (non-
+// decreasing because processing times are >= 0).  Ties of equal ready times land in one bucket
+// and are ordered by job in P4, so no assumption on distinct completions is needed.
+template <int G>
+__device__ __forceinline__ double group_min_d(double v) {
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        double o = __shfl_xor_sync(kFull, v, off, G);
+        v = (o < v) ? o : v;
+    }
+    return v;
+}
+
+template <int G>
+__device__ __forceinline__ int group_excl_scan(int v, int m, int& total) {
+    int x = v;
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, off, G);
+        if (m >= off) x += y;
+    }
+    total = __shfl_sync(kFull, x, G - 1, G);
+    return x - v;
+}
+
+struct BucketMap {
+    double lo, scale;
+    int nbd;
+    __device__ __forceinline__ int operator()(double key, int g) const {
+        const unsigned b = __double2uint_rz(__dmul_rn(__dsub_rn(key, lo), scale));
+        return g * nbd + (int)min(b, (unsigned)(nbd - 1));
+    }
+};
+
+__device__ __forceinline__ unsigned cnt_add(uint16_t* cnt, int idx) {
+    unsigned* w = reinterpret_cast<unsigned*>(cnt) + (idx >> 1);
+    const int sh = (idx & 1) * 16;
+    return (atomicAdd(w, 1u << sh) >> sh) & 0xFFFFu;
+}
+
+template <int G, bool SCHED>
+__global__ void __launch_bounds__(512) k_eval_bkt(DevInst I, EvalItems W, int groups_per_cta, BucketLayout BL) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int m = lane % G;
+    const int gid = threadIdx.x / G;
+    unsigned char* gb = smem + (size_t)gid * BL.bytes;
+    double* keys = reinterpret_cast<double*>(gb);
+    uint8_t* const row = gb + BL.off_row;
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(gb + BL.off_cnt);
+    uint16_t* scat = reinterpret_cast<uint16_t*>(gb + BL.off_scat);
+    uint16_t* fin = reinterpret_cast<uint16_t*>(gb + BL.off_fin);
+    const int J = I.J, S = I.S;
+    const long long n = W.n_dev ? *W.n_dev : W.n;
+
+    for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
+         base += (long long)gridDim.x * groups_per_cta) {
+        const long long item = base + gid;
+        const bool active = item < n;
+        const uint8_t* genes = nullptr;
+        if (active) {
+            genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
+            prefetch_row<G>(I, genes, 0, m, row);
+            for (int k = m; k < J; k += G) keys[I.rel_order[k]] = (double)k;  // stage-0 key: release rank
+        }
+        bool work = active;
+        double lo = 0.0, hi = (double)(J - 1);
+        for (int s = 0; s < S; ++s) {
+            const int Ms = I.M[s];
+            const int nbd = (BL.nbj + Ms - 1) / Ms;
+            const int nb = Ms * nbd;
+            BucketMap bm;
+            bm.lo = lo;
+            bm.nbd = nbd;
+            {
+                const double span = __dsub_rn(hi, lo);
+                // any positive scale keeps the map monotone; fp32 reciprocal (no fp64 divide)
+                bm.scale = (span > 0.0) ? (double)__fmul_rn((float)nbd, __frcp_rn((float)span)) : 0.0;
+            }
+            // clear the histogram (16 B stores)
+            uint4* c4 = reinterpret_cast<uint4*>(cnt);
+            const int nvec = (nb + 7) >> 3;
+            for (int v = m; v < nvec; v += G) c4[v] = make_uint4(0, 0, 0, 0);
+            __pipeline_wait_prior(0);  // gene row s has landed
+            __syncwarp();
+
+            // P1: histogram; out-of-range genes tracked as (key, job) = dispatch order
+            BadTrack bad;
+            bad.reset();
+            bool any_bad = false;
+            if (work) {
+#pragma unroll 4
+                for (int j = m; j < J; j += G) {
+                    const double k = keys[j];
+                    const int g = row[j];
+                    if (g < Ms) {
+                        const int idx = bm(k, g);
+                        atomicAdd(reinterpret_cast<unsigned*>(cnt) + (idx >> 1), 1u << ((idx & 1) * 16));
+                    } else {
+                        any_bad = true;
+                        bad.consider(k, j);
+                    }
+                }
+            }
+            if (__any_sync(kFull, any_bad)) {
+                double bc = bad.c;
+                int bj = bad.j;
+                group_min_key<G>(bc, bj);
+                if (work && bj != 0x7FFFFFFF) {
+                    work = false;
+                    if (m == 0 && W.err)
+                        atomicMin(W.err, ((unsigned long long)item << 32) | ((unsigned long long)s << 16) |
+                                             (unsigned long long)bj);
+                }
+            }
+            __syncwarp();
+
+            // P2: exclusive scan of the u16 histogram; lane m owns a contiguous run of vectors
+            {
+                const int per = (nvec + G - 1) / G;
+                const int v0 = m * per, v1 = min(v0 + per, nvec);
+                int sum = 0;
+                for (int v = v0; v < v1; ++v) {
+                    const uint4 x = c4[v];
+                    sum += (int)((x.x & 0xFFFF) + (x.x >> 16) + (x.y & 0xFFFF) + (x.y >> 16) + (x.z & 0xFFFF) +
+                                 (x.z >> 16) + (x.w & 0xFFFF) + (x.w >> 16));
+                }
+                int total;
+                unsigned run = (unsigned)group_excl_scan<G>(sum, m, total);
+                auto excl = [&run](unsigned w) {
+                    const unsigned a = w & 0xFFFF, b = w >> 16;
+                    const unsigned o = run | ((run + a) << 16);
+                    run += a + b;
+                    return o;
+                };
+                for (int v = v0; v < v1; ++v) {
+                    uint4 x = c4[v];
+                    x.x = excl(x.x);
+                    x.y = excl(x.y);
+                    x.z = excl(x.z);
+                    x.w = excl(x.w);
+                    c4[v] = x;
+                }
+            }
+            __syncwarp();
+
+            // P3: scatter to bucket slots
+            if (work) {
+#pragma unroll 4
+                for (int j = m; j < J; j += G) {
+                    const int idx = bm(keys[j], row[j]);
+                    scat[cnt_add(cnt, idx)] = (uint16_t)j;
+                }
+            }
+            __syncwarp();
+
+            // P4: exact order inside each bucket; cnt[idx] now holds the end of bucket idx.  Buckets
+            // hold ~2 jobs on average (uniform keys: Poisson), so the first kWin members are
+            // compared branch-free and only larger buckets take the loop.
+            if (work) {
+                constexpr int kWin = 4;
+#pragma unroll 2
+                for (int p = m; p < J; p += G) {
+                    const int j = scat[p];
+                    const double k = keys[j];
+                    const int idx = bm(k, row[j]);
+                    const int st = idx ? (int)cnt[idx - 1] : 0;
+                    const int en = cnt[idx];
+                    int r = 0;
+#pragma unroll
+                    for (int u = 0; u < kWin; ++u) {
+                        const int q = st + u;
+                        const int jq = scat[q < en ? q : p];
+                        r += (q < en && key_lt(keys[jq], jq, k, j)) ? 1 : 0;
+                    }
+                    for (int q = st + kWin; q < en; ++q) {
+                        const int jq = scat[q];
+                        r += key_lt(keys[jq], jq, k, j) ? 1 : 0;
+                    }
+                    fin[st + r] = (uint16_t)j;
+                }
+            }
+            __syncwarp();
+            // the row buffer is free: stage s+1's genes land during the recurrence
+            if (work && s + 1 < S) prefetch_row<G>(I, genes, s + 1, m, row);
+            if (work && s + 2 < S)
+                for (int v = m; v * 128 < I.Jpad; v += G)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(genes + (size_t)(s + 2) * I.Jpad + v * 128));
+
+            // P5: machine recurrence
+            double first = dinf(), avail = -dinf();
+            if (work && m < Ms) {
+                const int b0 = m * nbd;
+                const int begin = b0 ? (int)cnt[b0 - 1] : 0;
+                const int finish = cnt[b0 + nbd - 1];
+                const double* pcol = I.procT + (size_t)(I.stage_off[s] + m) * (J + 1);
+                double av = 0.0;
+                auto step = [&](int j, double r, double p) {
+                    const double start = (r < av) ? av : r;  // std::max(ready, avail)
+                    const double c = __dadd_rn(start, p);
+                    av = c;
+                    keys[j] = c;
+                    if (SCHED) {
+                        const int at = j * S + s;
+                        W.smachine[at] = m;
+                        W.sstart[at] = start;
+                        W.scomp[at] = c;
+                    }
+                };
+                // stage 0 reads release times (global), later stages the previous completions (smem)
+                auto run = [&](auto rel_tag) {
+                    constexpr bool REL = decltype(rel_tag)::value;
+                    auto ready = [&](int j) { return REL ? __ldg(I.release + j) : keys[j]; };
+                    int t = begin;
+                    if (t < finish) {  // first job: its completion is the machine's minimum
+                        const int j = fin[t];
+                        step(j, ready(j), __ldg(pcol + (unsigned)j));
+                        first = av;
+                        ++t;
+                    }
+                    // four jobs per round: their loads are independent of the recurrence
+                    for (; t + 3 < finish; t += 4) {
+                        const int j0 = fin[t], j1 = fin[t + 1], j2 = fin[t + 2], j3 = fin[t + 3];
+                        const double r0 = ready(j0), r1 = ready(j1), r2 = ready(j2), r3 = ready(j3);
+                        const double p0 = __ldg(pcol + (unsigned)j0), p1 = __ldg(pcol + (unsigned)j1);
+                        const double p2 = __ldg(pcol + (unsigned)j2), p3 = __ldg(pcol + (unsigned)j3);
+                        step(j0, r0, p0);
+                        step(j1, r1, p1);
+                        step(j2, r2, p2);
+                        step(j3, r3, p3);
+                    }
+                    for (; t < finish; ++t) {
+                        const int j = fin[t];
+                        step(j, ready(j), __ldg(pcol + (unsigned)j));
+                    }
+                };
+                if (s == 0)
+                    run(std::true_type{});
+                else
+                    run(std::false_type{});
+                if (finish > begin) avail = av;
+            }
+            lo = group_min_d<G>(first);
+            hi = group_max<G>(avail);
+            stage_barrier(I.cta_sync);
+        }
+        __pipeline_wait_prior(0);
+
+        // report_from_completions (model.cpp:107-120)
+        double mk = 0.0;
+        if (work) {
+            for (int j = m; j < J; j += G) {
+                const double c = keys[j];
+                mk = (mk < c) ? c : mk;
+                const double t = __dsub_rn(c, __ldg(I.due + j));
+                keys[j] = (0.0 < t) ? t : 0.0;
+            }
+        }
+        mk = group_max<G>(mk);
+        __syncwarp();
+        if (work && m == 0) {
+            double T = 0.0;
+            for (int j = 0; j < J; ++j) T = __dadd_rn(T, keys[j]);
+            const double obj = __dadd_rn(__dmul_rn(I.weight, T), mk);
+            const double f = __dsub_rn(I.emax, obj);
+            W.obj[item] = obj;
+            W.fit[item] = (f < 0.0) ? 0.0 : f;
             if (W.mk) W.mk[item] = mk;
             if (W.td) W.td[item] = T;
         }
@@ -1015,6 +1304,8 @@ int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
     (void)sm_count;
     cfg->G = G;
     cfg->gl = group_layout(I.J, I.Jpad, G);
+    cfg->bl = bucket_layout(I.J, I.Jpad, G, I.bshift);
+    if (I.algo == 1) cfg->gl.bytes = cfg->bl.bytes;  // bytes per group of the decoder in use
     const int max_smem = 227 * 1024;
     const size_t per_warp = (size_t)(32 / G) * cfg->gl.bytes;
     int warps = (int)std::min<size_t>(I.max_warps > 0 ? I.max_warps : 16, max_smem / per_warp);
@@ -1022,12 +1313,14 @@ int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
     cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
-    cudaError_t e = cudaFuncSetAttribute(k_eval<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false>;
+    const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true>;
+    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
     if (e != cudaSuccess) return -2;
-    e = cudaFuncSetAttribute(k_eval<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
     if (e != cudaSuccess) return -2;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_eval<G, false>, 32 * warps, cfg->smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, 32 * warps, cfg->smem);
     if (e != cudaSuccess || occ < 1) return -2;
     cfg->blocks_per_sm = occ;
     return 0;
@@ -1040,10 +1333,16 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
     const long long cap = (long long)cfg.blocks_per_sm * sm_count;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (schedule)
+    if (I.algo == 1) {
+        if (schedule)
+            k_eval_bkt<G, true><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.bl);
+        else
+            k_eval_bkt<G, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.bl);
+    } else if (schedule) {
         k_eval<G, true><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
-    else
+    } else {
         k_eval<G, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+    }
     return cudaGetLastError();
 }
 

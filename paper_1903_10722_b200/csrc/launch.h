@@ -78,6 +78,7 @@ struct WorkList {
 struct EvalConfig {
     int G, warps, groups_per_cta, blocks_per_sm;
     GroupLayout gl;
+    BucketLayout bl;
     size_t smem;
 };
 int eval_config(const DevInst& I, int sm_count, EvalConfig* cfg);

@@ -156,3 +156,73 @@ def test_full_size_sweep_properties(capi, orc):
         assert (r["objective"], r["fitness"], r["makespan"], r["total_tardiness"]) == (obj[i], fit[i], mk[i], td[i])
     want = oi.random_population(99, 12345, 1)[0]
     assert np.array_equal(b.download(12345, 1)[0], want)
+
+
+# ---- the bucket-sort decoder (K1b): forced on every shape, and chosen automatically for instances
+# whose processing times fall below ulp(horizon), where completions on a machine can tie
+
+@pytest.fixture
+def bucket(monkeypatch):
+    monkeypatch.setenv("FFSGA_EVAL_ALGO", "bucket")  # read when an instance is created
+
+
+@pytest.mark.parametrize("J,S,lo,hi", SHAPES)
+def test_bucket_decoder_bitwise(capi, orc, bucket, J, S, lo, hi):
+    d = synthetic(orc, J, S, lo, hi)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    pop = oi.random_population(7, 0, 200 if J * S <= 2000 else 50)
+    obj, fit, mk, td = inst.evaluate(pop, full=True)
+    eo, ef, em, et = oi.score_batch(pop, emax)
+    for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_bucket_decoder_ties_errors_schedule(capi, orc, bucket):
+    for seed in range(4):
+        d = orc.generate(40, 6, [2, 3, 4, 2, 3, 2], weight=1.0, seed=seed, integer_times=True)
+        oi = orc.instance(d)
+        emax = oi.estimate_emax()
+        pop = oi.random_population(seed, 0, 300)
+        obj, fit = capi.Instance.from_data(d, emax).evaluate(pop)
+        eo, ef, _, _ = oi.score_batch(pop, emax)
+        assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
+    d = micro(orc)
+    inst = capi.Instance.from_data(d, 211.0)
+    oi = orc.instance(d)
+    for genes in ([0, 1, 0, 0], [-1, 0, 0, 0], [0, 0, 5, 0], [0, 7, 0, 7]):
+        with pytest.raises(ValueError) as a:
+            inst.evaluate([genes])
+        with pytest.raises(ValueError) as b:
+            oi.score(genes, 211.0)
+        assert str(a.value).split(" (")[0] == str(b.value)
+    d = synthetic(orc, 50, 6)
+    oi = orc.instance(d)
+    inst = capi.Instance.from_data(d, oi.estimate_emax())
+    for g in oi.random_population(5, 0, 6):
+        m, s, c, rep = inst.decode(g)
+        e = oi.score(g, oi.estimate_emax(), schedule=True)
+        assert np.array_equal(m, e["machine"]) and np.array_equal(s, e["start"])
+        assert np.array_equal(c, e["completion"]) and rep["objective"] == e["objective"]
+
+
+def test_sub_ulp_processing_times(capi, orc):
+    """Release times near 2^53 with processing times below their ulp: start + p rounds back to
+    start, so completions on one machine tie.  The merge decoder cannot order such lists; the
+    instance runs on the bucket decoder automatically and still matches the reference."""
+    from pyoracle import InstanceData
+    rng = np.random.default_rng(3)
+    J, S, M = 60, 4, [2, 3, 2, 3]
+    proc = rng.choice([0.25, 0.5, 1.0, 3.0, 8.0], size=(J, sum(M)))
+    release = 2.0 ** 53 + rng.integers(0, 40, J).astype(np.float64) * 2.0
+    due = release + 50.0
+    d = InstanceData(J, S, M, proc, release, due, 0.5)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    pop = oi.random_population(11, 0, 400)
+    obj, fit, mk, td = inst.evaluate(pop, full=True)
+    eo, ef, em, et = oi.score_batch(pop, emax)
+    for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
