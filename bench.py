@@ -38,6 +38,7 @@ METRIC = "FFS makespan evals/sec & GA generations/sec at 1/2/4/8 B200 vs CPU ref
 J, S, LO, HI, GEN_SEED, WEIGHT = 500, 20, 2, 8, 7, 100.0
 COUPLES, ISLAND_POP, GRID = 4, 8192, (128, 64)
 RUN_SEED, GAP, THETA = 1, 500, 1.0
+E2E_RUNS = 3
 SWEEP_N = 1 << 20
 
 
@@ -320,23 +321,45 @@ def main():
         except Exception:
             pass
         achieved = algo_bytes / (eval_ms / 1e3) / 1e9 if eval_ms > 0 else 0.0
+        issue = None  # K1 is issue/latency bound: the integer-issue roofline from the same capture
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_ncu.json")) as f:
+                for k in json.load(f)["kernels"]:
+                    if "k_eval<8, 0>" in k["kernel"]:
+                        ia = k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0
+                        issue = {"bound": "issue", "frac": ia, "unit": "warp instructions/cycle/SMSP",
+                                 "achieved": ia, "peak": 1.0,
+                                 "warps_per_sm": k["sm__warps_active.avg.per_cycle_active"],
+                                 "source": "profiles/r1_ncu.json (ncu --set full of this step's K1 launch)"}
+                        break
+        except Exception:
+            pass
 
         # e2e: the public API call a user makes (instance upload, island init, K generations,
-        # traces + champion back to the host), wall clock
-        barrier()
-        t0 = time.perf_counter()
-        inst2, emax2 = make_instance()
-        cfg2 = IslandConfig(couples=COUPLES, island_population=ISLAND_POP, generations=args.steps,
-                            migration_gap=GAP, theta=THETA, seed=RUN_SEED, grid_shape=GRID)
-        model2 = IslandModel(instance_arrays(inst2), emax2, cfg2, comm, device=local)
-        res = model2.run()
-        barrier()
-        e2e_s = time.perf_counter() - t0
-        if comm is not None:
-            e2e_s = float(comm.allgather(np.array([e2e_s]))[:, 0].max())
+        # traces + champion back to the host), wall clock; median of E2E_RUNS independent runs
+        runs = []
+        for _ in range(E2E_RUNS):
+            barrier()
+            t0 = time.perf_counter()
+            inst2, emax2 = make_instance()
+            cfg2 = IslandConfig(couples=COUPLES, island_population=ISLAND_POP, generations=args.steps,
+                                migration_gap=GAP, theta=THETA, seed=RUN_SEED, grid_shape=GRID)
+            model2 = IslandModel(instance_arrays(inst2), emax2, cfg2, comm, device=local)
+            t1 = time.perf_counter()
+            res = model2.run()
+            barrier()
+            t2 = time.perf_counter()
+            runs.append((t2 - t0, t1 - t0, t2 - t1))
+            del model2
+        if comm is not None:  # max over ranks, per run
+            agg = comm.allgather(np.array([r[0] for r in runs]))
+            runs = [(float(agg[:, i].max()),) + runs[i][1:] for i in range(len(runs))]
+        runs.sort()
+        e2e_s = runs[len(runs) // 2][0]
+        e2e_parts = {"instance_and_init_s": runs[len(runs) // 2][1], "run_s": runs[len(runs) // 2][2],
+                     "runs_total_s": [r[0] for r in runs]}
         h2d = (L * sum(synthetic_machines(J, S)) + 2 * J) * 8 + S * 4
         d2h = 2 * COUPLES * args.steps * 8 + L * 4 + 5 * 8
-        del model2
 
         sweep = None
         if world == 1 and not args.no_sweep:
@@ -364,11 +387,14 @@ def main():
                              "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1_traffic.json)",
                              "algorithmic_bytes_per_launch": algo_bytes / max(1, eval_n),
                              "algorithmic_bytes_per_eval": L + 16,
+                             "issue_roofline": issue,
                              "note": "decoder is latency/issue bound (fp64 max/add chains + smem list "
                                      "merges); see profiles/ for issue-active and DRAM counters"},
                 "e2e": {"value": args.steps / e2e_s, "unit": "generations/s",
                         "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-                        "what": "generate instance + IslandModel init + run(K generations) + traces/champion D2H",
+                        "what": "generate instance + IslandModel init + run(K generations) + traces/champion D2H; "
+                                "median of %d runs in one process" % E2E_RUNS,
+                        "parts": e2e_parts,
                         "best_objective": res.best_report["objective"]},
                 "gpu_launches": int(l1 - l0),
                 "clocks": clk.summary(),

@@ -50,6 +50,24 @@ int guard(F&& f) {
     }
 }
 
+// Device memory comes from the device's stream-ordered pool with an unbounded release
+// threshold: freed island/batch buffers stay mapped and the next instance or island reuses them
+// without a new mapping (a solver process that builds several models pays the mapping once).
+// Allocation and release keep cudaMalloc/cudaFree's synchronous semantics.
+inline void pool_setup_once() {
+    static std::once_flag once[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    });
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -58,14 +76,19 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaDeviceSynchronize();  // every use of the buffer has completed (cudaFree semantics)
+            cudaFreeAsync(p, 0);
+        }
         p = nullptr;
         bytes = 0;
     }
     void alloc(size_t n) {
         release();
         if (n == 0) n = 16;
-        cudaError_t e = cudaMalloc(&p, n);
+        pool_setup_once();
+        cudaError_t e = cudaMallocAsync(&p, n, 0);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(0);  // usable from every stream
         if (e != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
