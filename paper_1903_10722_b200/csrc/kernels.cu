@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
     uint8_t* const row_a = gb + GL.off_row;
     const int J = I.J, S = I.S;
     const int END = J;
-    const long long n = W.n_dev ? *W.n_dev : W.n;
+    const long long n = W.n_dev ? *W.n_dev + W.n : W.n;  // fused GA list: n cells + device count
 
     // all groups of the CTA share the item loop (CTA-uniform bounds: stage barriers)
     for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(512) k_eval_bkt(DevInst I, EvalItems W, int gr
     uint16_t* scat = reinterpret_cast<uint16_t*>(gb + BL.off_scat);
     uint16_t* fin = reinterpret_cast<uint16_t*>(gb + BL.off_fin);
     const int J = I.J, S = I.S;
-    const long long n = W.n_dev ? *W.n_dev : W.n;
+    const long long n = W.n_dev ? *W.n_dev + W.n : W.n;  // fused GA list: n cells + device count
 
     for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
          base += (long long)gridDim.x * groups_per_cta) {
@@ -1300,7 +1300,7 @@ inline unsigned blocks_for(long long threads, int per_block) {
 }
 
 template <int G>
-int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
+int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg) {
     (void)sm_count;
     cfg->G = G;
     cfg->gl = group_layout(I.J, I.Jpad, G);
@@ -1308,16 +1308,18 @@ int eval_config_g(const DevInst& I, int sm_count, EvalConfig* cfg) {
     if (I.algo == 1) cfg->gl.bytes = cfg->bl.bytes;  // bytes per group of the decoder in use
     const int max_smem = 227 * 1024;
     const size_t per_warp = (size_t)(32 / G) * cfg->gl.bytes;
-    int warps = (int)std::min<size_t>(I.max_warps > 0 ? I.max_warps : 16, max_smem / per_warp);
+    int warps = (int)std::min<size_t>(warps_cap > 0 ? warps_cap : 16, max_smem / per_warp);
     if (warps < 1) return -1;
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
     cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
     const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false>;
     const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true>;
-    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    // the opt-in ceiling, not this config's size: configs of other instances (other J) and the
+    // joint-step config share the kernel's attribute
+    cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e != cudaSuccess) return -2;
-    e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem);
+    e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e != cudaSuccess) return -2;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, 32 * warps, cfg->smem);
@@ -1348,11 +1350,11 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
 
 }  // namespace
 
-int eval_config(const DevInst& I, int sm_count, EvalConfig* cfg) {
-    if (I.maxM <= 4) return eval_config_g<4>(I, sm_count, cfg);
-    if (I.maxM <= 8) return eval_config_g<8>(I, sm_count, cfg);
-    if (I.maxM <= 16) return eval_config_g<16>(I, sm_count, cfg);
-    if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, cfg);
+int eval_config(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg) {
+    if (I.maxM <= 4) return eval_config_g<4>(I, sm_count, warps_cap, cfg);
+    if (I.maxM <= 8) return eval_config_g<8>(I, sm_count, warps_cap, cfg);
+    if (I.maxM <= 16) return eval_config_g<16>(I, sm_count, warps_cap, cfg);
+    if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, warps_cap, cfg);
     return -3;
 }
 

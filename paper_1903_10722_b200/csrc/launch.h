@@ -11,7 +11,7 @@ namespace ffsga_dev {
 // Batch of chromosomes for the decoder (K1 / K7).
 struct EvalItems {
     const long long* n_dev;        // item count on device (joint GA step) or nullptr
-    long long n;                   // item count when n_dev == nullptr
+    long long n;                   // item count (plus *n_dev when set)
     const uint8_t* base;           // implicit rows: base + i * stride
     long long stride;
     const uint8_t* const* ptrs;    // explicit per-item row blocks (GA work list) or nullptr
@@ -81,7 +81,8 @@ struct EvalConfig {
     BucketLayout bl;
     size_t smem;
 };
-int eval_config(const DevInst& I, int sm_count, EvalConfig* cfg);
+// warps_cap: CTA size cap in warps (0 = 16); the CTA is also capped by shared memory
+int eval_config(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg);
 cudaError_t launch_eval(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,
                         int sm_count, bool schedule, cudaStream_t st);
 // random rows: item i seeded with seed_i = per_item ? derive_seed(base, first + i) : base and
