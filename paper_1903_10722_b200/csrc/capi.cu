@@ -148,7 +148,9 @@ struct ffsga_cuda_instance_t {
     EvalConfig ec{};       // standalone batches: full-size CTAs
     EvalConfig ec_step{};  // joint GA step: half-size CTAs (two decoder launches share the SMs)
     cudaStream_t stream = nullptr;
-    cudaStream_t stream2 = nullptr;  // pseudo islands of a joint step run beside the cellular ones
+    std::vector<cudaStream_t> side;      // joint step: streams of step groups 1.. (group 0: stream)
+    std::vector<cudaEvent_t> side_join;
+    int step_split = 1;                  // joint step: groups per island kind (measured best at C3)
     cudaEvent_t fork = nullptr, join = nullptr;
     // CUDA graph of `graph_chunk` generations of the last joint step (relaunched while the
     // island set and the work-list buffers are unchanged)
@@ -164,7 +166,6 @@ struct ffsga_cuda_instance_t {
     DevBuf mg_keys0, mg_keys1, mg_idx0, mg_idx_a, mg_idx_b, mg_temp;
     // timing: event pairs recorded around launches, resolved lazily (no sync in the timed path)
     bool timing = false;
-    bool fused_eval = false;  // joint step: one decoder launch over cellular and pseudo children
     double t_ms[3] = {0, 0, 0};
     long long t_n[3] = {0, 0, 0};
     struct Pending {
@@ -182,7 +183,8 @@ struct ffsga_cuda_instance_t {
     ~ffsga_cuda_instance_t() {
         cudaSetDevice(device);
         if (stream) cudaStreamDestroy(stream);
-        if (stream2) cudaStreamDestroy(stream2);
+        for (auto s : side) cudaStreamDestroy(s);
+        for (auto e : side_join) cudaEventDestroy(e);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -459,8 +461,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
             }
         }
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
-        I->fused_eval = false;
-        if (const char* v = std::getenv("FFSGA_STEP_FUSED")) I->fused_eval = std::atoi(v) != 0;
+        if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
         int rc = eval_config(d, I->sm_count, d.max_warps, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
@@ -473,14 +474,13 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         rc = eval_config(d, I->sm_count, step_warps, &I->ec_step);
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&I->stream2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&I->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I->join, cudaEventDisableTiming));
         CK(cudaEventCreate(&I->ev0));
         CK(cudaEventCreate(&I->ev1));
         CK(cudaEventCreate(&I->st0));
         CK(cudaEventCreate(&I->st1));
-        I->wl_count.alloc(2 * sizeof(long long));  // [0] cellular items, [1] crossed pseudo members
+        I->wl_count.alloc(2 * sizeof(long long));  // one item counter per joint-step group (grown on demand)
         I->eval_total.alloc(sizeof(unsigned long long));
         CK(cudaMemset(I->eval_total.p, 0, sizeof(unsigned long long)));
         *out = hold.release();
@@ -1249,10 +1249,18 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             if (!pseudos[i] || pseudos[i]->inst != I) fail(FFSGA_ERR_ARG, "step: islands must share one instance");
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
-        // descriptors of this joint step: work items = every cell, then crossed pseudo members
+        // Descriptors of this joint step.  The islands are split into step groups (up to
+        // step_split contiguous groups of each kind) and every group runs its own breed ->
+        // evaluate -> commit chain on its own stream: groups never read each other between
+        // rendezvous, so the GPU overlaps the integer-bound breeding of one group with the
+        // latency-bound decoding of another and fills the tail of every decoder launch.
+        // Work-list items: every cell in island order, then per pseudo group a region of
+        // 2 x its pairs for the crossed members.
+        const int split = std::max(1, I->step_split);
+        const int gc = nc ? std::min(nc, split) : 0, gp = np ? std::min(np, split) : 0;
         std::vector<CellIsland> cd(nc);
         std::vector<PseudoIsland> pd(np);
-        long long n_cells = 0, n_pairs = 0;
+        std::vector<long long> cell_base(nc + 1, 0), pair_base(np + 1, 0);
         for (int i = 0; i < nc; ++i) {
             auto* c = cells[i];
             if (c->trace_cap < generations) {
@@ -1261,9 +1269,8 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             }
             c->d.trace = c->trace.as<double>();
             cd[i] = c->d;
-            cd[i].item0 = n_cells;
-            cd[i].cell0 = n_cells;
-            n_cells += c->n;
+            cd[i].item0 = cell_base[i];
+            cell_base[i + 1] = cell_base[i] + c->n;
             CK(cudaMemcpyAsync(&c->st.as<IslandState>()->seg_start, &c->gen, sizeof(unsigned long long),
                                cudaMemcpyHostToDevice, I->stream));
         }
@@ -1275,102 +1282,113 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             }
             p->d.trace = p->trace.as<double>();
             pd[i] = p->d;
-            pd[i].pair0 = n_pairs;
-            n_pairs += p->n / 2;
+            pair_base[i + 1] = pair_base[i] + p->n / 2;
             CK(cudaMemcpyAsync(&p->st.as<IslandState>()->seg_start, &p->gen, sizeof(unsigned long long),
                                cudaMemcpyHostToDevice, I->stream));
+        }
+        const long long n_cells = cell_base[nc], n_pairs = pair_base[np];
+        struct Group {
+            bool cell;
+            int i0, i1;
+            long long units;  // cells, or pairs
+            long long item0;  // first work-list item of the group
+        };
+        std::vector<Group> groups;
+        for (int g = 0; g < gc; ++g) {
+            const int i0 = (int)((long long)g * nc / gc), i1 = (int)((long long)(g + 1) * nc / gc);
+            for (int i = i0; i < i1; ++i) cd[i].cell0 = cell_base[i] - cell_base[i0];  // launch-relative
+            groups.push_back({true, i0, i1, cell_base[i1] - cell_base[i0], cell_base[i0]});
+        }
+        for (int g = 0; g < gp; ++g) {
+            const int i0 = (int)((long long)g * np / gp), i1 = (int)((long long)(g + 1) * np / gp);
+            for (int i = i0; i < i1; ++i) pd[i].pair0 = pair_base[i] - pair_base[i0];
+            groups.push_back({false, i0, i1, pair_base[i1] - pair_base[i0], n_cells + 2 * pair_base[i0]});
         }
         const long long cap = n_cells + 2 * n_pairs;
         I->wl_ptrs.ensure(sizeof(void*) * cap);
         I->wl_obj.ensure(sizeof(double) * cap);
         I->wl_fit.ensure(sizeof(double) * cap);
         I->wl_scratch.ensure(std::max<size_t>(1, (size_t)(2 * n_pairs) * I->block()));
+        I->wl_count.ensure(sizeof(long long) * std::max<size_t>(2, groups.size()));
         I->cell_desc.ensure(sizeof(CellIsland) * std::max(1, nc));
         I->pseudo_desc.ensure(sizeof(PseudoIsland) * std::max(1, np));
         if (nc) CK(cudaMemcpyAsync(I->cell_desc.p, cd.data(), sizeof(CellIsland) * nc, cudaMemcpyHostToDevice, I->stream));
         if (np) CK(cudaMemcpyAsync(I->pseudo_desc.p, pd.data(), sizeof(PseudoIsland) * np, cudaMemcpyHostToDevice, I->stream));
-        // Cellular and pseudo islands never read each other between rendezvous, so each kind
-        // runs its breed -> evaluate -> commit chain on its own stream and the GPU overlaps the
-        // integer-bound breeding of one with the latency-bound decoding of the other.
-        WorkList wc{}, wp{};
-        wc.ptrs = I->wl_ptrs.as<const uint8_t*>();
-        wc.obj = I->wl_obj.as<double>();
-        wc.fit = I->wl_fit.as<double>();
-        wc.count = I->wl_count.as<long long>();
-        wc.total = I->eval_total.as<unsigned long long>();
-        wp = wc;
-        wp.ptrs += n_cells;
-        wp.obj += n_cells;
-        wp.fit += n_cells;
-        wp.count = I->wl_count.as<long long>() + 1;
-        wp.scratch = I->wl_scratch.as<uint8_t>();
-        wp.scratch0 = 0;
         const CellIsland* cdev = I->cell_desc.as<CellIsland>();
         const PseudoIsland* pdev = I->pseudo_desc.as<PseudoIsland>();
-        EvalItems Wc{}, Wp{};
-        Wc.n = n_cells;
-        Wc.ptrs = wc.ptrs;
-        Wc.obj = wc.obj;
-        Wc.fit = wc.fit;
-        Wp.n_dev = wp.count;
-        Wp.ptrs = wp.ptrs;
-        Wp.obj = wp.obj;
-        Wp.fit = wp.fit;
-        // fused: one decoder launch over both kinds' children (cells, then crossed pseudo
-        // members); breeding and commits still run side by side on the two streams
-        const bool fused = nc && np && I->fused_eval;
-        EvalItems Wf = Wc;
-        Wf.n_dev = wp.count;  // n = n_cells + crossed pseudo members (device count)
-        auto enqueue_fused = [&](int gens, bool timed) {
-            for (int g = 0; g < gens; ++g) {
-                auto run = [&](int slot, cudaStream_t st, auto fn) {
-                    if (timed)
-                        I->timed_on(slot, st, fn);
-                    else
-                        fn();
-                };
-                CK(cudaEventRecord(I->fork, I->stream));
-                CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
-                run(1, I->stream, [&] { CK(launch_breed(I->d, cdev, nc, n_cells, nullptr, 0, 0, wc, I->stream)); });
-                run(1, I->stream2, [&] { CK(launch_breed(I->d, nullptr, 0, 0, pdev, np, n_pairs, wp, I->stream2)); });
-                CK(cudaEventRecord(I->join, I->stream2));
-                CK(cudaStreamWaitEvent(I->stream, I->join, 0));
-                run(0, I->stream, [&] { CK(launch_eval(I->d, I->ec, Wf, n_cells + 2 * n_pairs, I->sm_count, false, I->stream)); });
-                CK(cudaEventRecord(I->fork, I->stream));
-                CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
-                run(2, I->stream, [&] { CK(launch_commit(I->d, cdev, nc, nullptr, 0, wc, I->stream)); });
-                run(2, I->stream2, [&] { CK(launch_commit(I->d, nullptr, 0, pdev, np, wp, I->stream2)); });
-                CK(cudaEventRecord(I->join, I->stream2));
-                CK(cudaStreamWaitEvent(I->stream, I->join, 0));
-            }
+        // group 0 runs on the instance stream, the others on side streams forked from it
+        while (I->side.size() + 1 < groups.size()) {
+            cudaStream_t s;
+            cudaEvent_t e;
+            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            I->side.push_back(s);
+            I->side_join.push_back(e);
+        }
+        struct Chain {
+            cudaStream_t st;
+            WorkList w;
+            EvalItems E;
         };
+        std::vector<Chain> chains(groups.size());
+        const uint8_t** ptrs = I->wl_ptrs.as<const uint8_t*>();
+        double* wobj = I->wl_obj.as<double>();
+        double* wfit = I->wl_fit.as<double>();
+        for (size_t k = 0; k < groups.size(); ++k) {
+            const Group& G = groups[k];
+            Chain& ch = chains[k];
+            ch.st = k == 0 ? I->stream : I->side[k - 1];
+            WorkList w{};
+            w.count = I->wl_count.as<long long>() + k;
+            w.total = I->eval_total.as<unsigned long long>();
+            EvalItems E{};
+            E.ptrs = ptrs + G.item0;
+            E.obj = wobj + G.item0;
+            E.fit = wfit + G.item0;
+            if (G.cell) {  // breed and commit index the global list through each island's item0
+                w.ptrs = ptrs;
+                w.obj = wobj;
+                w.fit = wfit;
+                E.n = G.units;
+            } else {  // pseudo slots are group-relative (counter from 0, scratch region of the group)
+                w.ptrs = ptrs + G.item0;
+                w.obj = wobj + G.item0;
+                w.fit = wfit + G.item0;
+                w.scratch = I->wl_scratch.as<uint8_t>() + (size_t)(G.item0 - n_cells) * I->block();
+                w.scratch0 = 0;
+                E.n_dev = w.count;
+            }
+            ch.w = w;
+            ch.E = E;
+        }
         auto enqueue = [&](int gens, bool timed) {
-            if (fused) return enqueue_fused(gens, timed);
             CK(cudaEventRecord(I->fork, I->stream));
-            CK(cudaStreamWaitEvent(I->stream2, I->fork, 0));
+            for (size_t k = 1; k < chains.size(); ++k) CK(cudaStreamWaitEvent(chains[k].st, I->fork, 0));
             for (int g = 0; g < gens; ++g) {
-                if (nc) {
-                    auto b = [&] { CK(launch_breed(I->d, cdev, nc, n_cells, nullptr, 0, 0, wc, I->stream)); };
-                    auto e = [&] { CK(launch_eval(I->d, I->ec_step, Wc, n_cells, I->sm_count, false, I->stream)); };
-                    auto c = [&] { CK(launch_commit(I->d, cdev, nc, nullptr, 0, wc, I->stream)); };
+                for (size_t k = 0; k < chains.size(); ++k) {
+                    const Group& G = groups[k];
+                    const Chain& ch = chains[k];
+                    const int ni = G.i1 - G.i0;
+                    auto b = [&] {
+                        if (G.cell)
+                            CK(launch_breed(I->d, cdev + G.i0, ni, G.units, nullptr, 0, 0, ch.w, ch.st));
+                        else
+                            CK(launch_breed(I->d, nullptr, 0, 0, pdev + G.i0, ni, G.units, ch.w, ch.st));
+                    };
+                    auto e = [&] {
+                        CK(launch_eval(I->d, I->ec_step, ch.E, G.cell ? G.units : 2 * G.units, I->sm_count, false,
+                                       ch.st));
+                    };
+                    auto c = [&] {
+                        if (G.cell)
+                            CK(launch_commit(I->d, cdev + G.i0, ni, nullptr, 0, ch.w, ch.st));
+                        else
+                            CK(launch_commit(I->d, nullptr, 0, pdev + G.i0, ni, ch.w, ch.st));
+                    };
                     if (timed) {
-                        I->timed_on(1, I->stream, b);
-                        I->timed_on(0, I->stream, e);
-                        I->timed_on(2, I->stream, c);
-                    } else {
-                        b();
-                        e();
-                        c();
-                    }
-                }
-                if (np) {
-                    auto b = [&] { CK(launch_breed(I->d, nullptr, 0, 0, pdev, np, n_pairs, wp, I->stream2)); };
-                    auto e = [&] { CK(launch_eval(I->d, I->ec_step, Wp, 2 * n_pairs, I->sm_count, false, I->stream2)); };
-                    auto c = [&] { CK(launch_commit(I->d, nullptr, 0, pdev, np, wp, I->stream2)); };
-                    if (timed) {
-                        I->timed_on(1, I->stream2, b);
-                        I->timed_on(0, I->stream2, e);
-                        I->timed_on(2, I->stream2, c);
+                        I->timed_on(1, ch.st, b);
+                        I->timed_on(0, ch.st, e);
+                        I->timed_on(2, ch.st, c);
                     } else {
                         b();
                         e();
@@ -1378,10 +1396,12 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                     }
                 }
             }
-            CK(cudaEventRecord(I->join, I->stream2));
-            CK(cudaStreamWaitEvent(I->stream, I->join, 0));
+            for (size_t k = 1; k < chains.size(); ++k) {
+                CK(cudaEventRecord(I->side_join[k - 1], chains[k].st));
+                CK(cudaStreamWaitEvent(I->stream, I->side_join[k - 1], 0));
+            }
         };
-        const long long per_gen = (nc ? 4 : 0) + (np ? 4 : 0) - (fused ? 1 : 0);
+        const long long per_gen = 4 * (long long)groups.size();
         // graphs pay off when a generation is launch bound (small islands); capturing costs
         // ~0.1 s, so large work lists run plain launches
         const bool use_graph = !I->timing && generations >= 2 && cap <= 16384 && !std::getenv("FFSGA_NO_GRAPH");
@@ -1390,7 +1410,8 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             // the generation sequence is launch-bound for small islands: capture a chunk of
             // generations once (device-side generation counters make it replayable)
             const int chunk = std::min(generations, 16);
-            const std::vector<const void*> key = {cdev, pdev, wc.ptrs, wc.obj, wp.scratch, I->wl_count.p,
+            const std::vector<const void*> key = {cdev, pdev, (const void*)ptrs, (const void*)wobj,
+                                                  I->wl_scratch.p, I->wl_count.p, (const void*)groups.size(),
                                                   (const void*)(intptr_t)nc, (const void*)(intptr_t)np,
                                                   (const void*)(intptr_t)n_cells, (const void*)(intptr_t)n_pairs,
                                                   (const void*)(intptr_t)chunk};
