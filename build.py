@@ -9,6 +9,7 @@ Outputs (git-ignored, shipped to the GPU box by the gpurun snapshot):
     paper_1903_10722_b200/libffsga_cuda.so     kernels + C ABI (include/ffsga_cuda.h)
     paper_1903_10722_b200/libffsga.so          C++ API mirror of the reference (namespace ffsga)
     paper_1903_10722_b200/_core*.so            pybind11 module with the reference's Python API
+    paper_1903_10722_b200/bin/ffsga            command-line front end (reference tools/main.cpp)
     oracle/liboracle.so, oracle/_ref/*.so      checkers (oracle/Makefile)
 """
 from __future__ import annotations
@@ -96,6 +97,22 @@ def build_host(force=False):
     return lib
 
 
+def build_cli(force=False):
+    """The command-line front end (reference proj/tools/main.cpp) -> paper_1903_10722_b200/bin/ffsga."""
+    src = os.path.join(CSRC, "tools", "ffsga_cli.cpp")
+    if not os.path.exists(src):
+        return None
+    hostdir = os.path.join(CSRC, "host")
+    out = os.path.join(PKG, "bin", "ffsga")
+    lib = os.path.join(PKG, "libffsga.so")
+    if force or _newer(out, [src, lib] + _headers(hostdir)):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        _run([CXX, "-std=c++20", "-O2", "-ffp-contract=off", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+              "-I" + hostdir, "-I" + NLOHMANN, src, "-L" + PKG, "-lffsga", "-lffsga_cuda",
+              "-Wl,-rpath,$ORIGIN/..", "-o", out])
+    return out
+
+
 def build_oracle(force=False):
     args = ["make", "-s", "-f", os.path.join(ROOT, "oracle", "Makefile")]
     if force:
@@ -110,6 +127,7 @@ def main(argv=None):
     a = ap.parse_args(argv)
     build_cuda(a.force)
     build_host(a.force)
+    build_cli(a.force)
     if not a.skip_oracle:
         build_oracle(a.force)
 

@@ -109,7 +109,10 @@ def test_pseudo_steps_match_oracle(capi, orc, J, S, lo, hi, n, xr):
         assert tp[0, 0] == op.archive()[2]
 
 
-def test_joint_step_equals_separate(capi, orc):
+@pytest.mark.parametrize("split", ["1", "2", "3"])
+def test_joint_step_equals_separate(capi, orc, monkeypatch, split):
+    # step groups (one stream per group of islands) must not change any result
+    monkeypatch.setenv("FFSGA_STEP_SPLIT", split)  # read when the instance is created
     d = synthetic(orc, 40, 6, 2, 6)
     oi = orc.instance(d)
     emax = oi.estimate_emax()
