@@ -462,7 +462,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         }
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
-        int rc = eval_config(d, I->sm_count, d.max_warps, &I->ec);
+        int rc = eval_config(d, I->sm_count, d.max_warps, true, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         // The joint GA step runs the cellular and the pseudo decoder launches side by side on two
@@ -471,7 +471,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         // (small CTAs of large instances -- J = 1000: 4 warps -- gain nothing: kept whole)
         int step_warps = I->ec.warps >= 6 ? I->ec.warps / 2 : I->ec.warps;
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
-        rc = eval_config(d, I->sm_count, step_warps, &I->ec_step);
+        rc = eval_config(d, I->sm_count, step_warps, false, &I->ec_step);
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&I->fork, cudaEventDisableTiming));
