@@ -151,6 +151,7 @@ struct ffsga_cuda_instance_t {
     std::vector<cudaStream_t> side;      // joint step: streams of step groups 1.. (group 0: stream)
     std::vector<cudaEvent_t> side_join;
     int step_split = 1;                  // joint step: groups per island kind (measured best at C3)
+    int step_mix = 0;                    // joint step: > 0 = that many groups holding both kinds
     cudaEvent_t fork = nullptr, join = nullptr;
     // CUDA graph of `graph_chunk` generations of the last joint step (relaunched while the
     // island set and the work-list buffers are unchanged)
@@ -462,6 +463,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         }
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
+        if (const char* v = std::getenv("FFSGA_STEP_MIX")) I->step_mix = std::max(0, std::atoi(v));
         int rc = eval_config(d, I->sm_count, d.max_warps, true, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
@@ -1287,22 +1289,37 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                                cudaMemcpyHostToDevice, I->stream));
         }
         const long long n_cells = cell_base[nc], n_pairs = pair_base[np];
+        // A step group owns a range of cellular islands [c0, c1) and of pseudo islands [p0, p1)
+        // and a work-list region: its cells first, then its crossed pseudo members (slots from
+        // the group counter); every index inside the group's kernels is group-relative.
         struct Group {
-            bool cell;
-            int i0, i1;
-            long long units;  // cells, or pairs
-            long long item0;  // first work-list item of the group
+            int c0, c1, p0, p1;
+            long long cells, pairs;  // units of the group
+            long long item0, srow0;  // first work-list item, first pseudo scratch row
         };
         std::vector<Group> groups;
-        for (int g = 0; g < gc; ++g) {
-            const int i0 = (int)((long long)g * nc / gc), i1 = (int)((long long)(g + 1) * nc / gc);
-            for (int i = i0; i < i1; ++i) cd[i].cell0 = cell_base[i] - cell_base[i0];  // launch-relative
-            groups.push_back({true, i0, i1, cell_base[i1] - cell_base[i0], cell_base[i0]});
-        }
-        for (int g = 0; g < gp; ++g) {
-            const int i0 = (int)((long long)g * np / gp), i1 = (int)((long long)(g + 1) * np / gp);
-            for (int i = i0; i < i1; ++i) pd[i].pair0 = pair_base[i] - pair_base[i0];
-            groups.push_back({false, i0, i1, pair_base[i1] - pair_base[i0], n_cells + 2 * pair_base[i0]});
+        auto add_group = [&](int c0, int c1, int p0, int p1) {
+            Group G{c0, c1, p0, p1, cell_base[c1] - cell_base[c0], pair_base[p1] - pair_base[p0], 0, 0};
+            if (G.cells + G.pairs == 0) return;
+            if (!groups.empty()) {
+                const Group& L = groups.back();
+                G.item0 = L.item0 + L.cells + 2 * L.pairs;
+                G.srow0 = L.srow0 + 2 * L.pairs;
+            }
+            for (int i = c0; i < c1; ++i) cd[i].item0 = cd[i].cell0 = cell_base[i] - cell_base[c0];
+            for (int i = p0; i < p1; ++i) pd[i].pair0 = pair_base[i] - pair_base[p0];
+            groups.push_back(G);
+        };
+        if (I->step_mix > 0) {  // mixed groups: each takes a share of both kinds
+            const int S = std::max(1, std::min(I->step_mix, std::max(nc, np)));
+            for (int g = 0; g < S; ++g)
+                add_group((int)((long long)g * nc / S), (int)((long long)(g + 1) * nc / S),
+                          (int)((long long)g * np / S), (int)((long long)(g + 1) * np / S));
+        } else {  // kind groups: cellular islands in gc groups, pseudo islands in gp groups
+            for (int g = 0; g < gc; ++g)
+                add_group((int)((long long)g * nc / gc), (int)((long long)(g + 1) * nc / gc), 0, 0);
+            for (int g = 0; g < gp; ++g)
+                add_group(0, 0, (int)((long long)g * np / gp), (int)((long long)(g + 1) * np / gp));
         }
         const long long cap = n_cells + 2 * n_pairs;
         I->wl_ptrs.ensure(sizeof(void*) * cap);
@@ -1339,25 +1356,18 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             Chain& ch = chains[k];
             ch.st = k == 0 ? I->stream : I->side[k - 1];
             WorkList w{};
-            w.count = I->wl_count.as<long long>() + k;
+            w.ptrs = ptrs + G.item0;
+            w.obj = wobj + G.item0;
+            w.fit = wfit + G.item0;
+            w.count = I->wl_count.as<long long>() + k;  // gen-begin sets it to the group's cells
             w.total = I->eval_total.as<unsigned long long>();
+            w.scratch = I->wl_scratch.as<uint8_t>() + (size_t)G.srow0 * I->block();
+            w.scratch0 = G.cells;  // pseudo slot s -> scratch row s - cells
             EvalItems E{};
-            E.ptrs = ptrs + G.item0;
-            E.obj = wobj + G.item0;
-            E.fit = wfit + G.item0;
-            if (G.cell) {  // breed and commit index the global list through each island's item0
-                w.ptrs = ptrs;
-                w.obj = wobj;
-                w.fit = wfit;
-                E.n = G.units;
-            } else {  // pseudo slots are group-relative (counter from 0, scratch region of the group)
-                w.ptrs = ptrs + G.item0;
-                w.obj = wobj + G.item0;
-                w.fit = wfit + G.item0;
-                w.scratch = I->wl_scratch.as<uint8_t>() + (size_t)(G.item0 - n_cells) * I->block();
-                w.scratch0 = 0;
-                E.n_dev = w.count;
-            }
+            E.ptrs = w.ptrs;
+            E.obj = w.obj;
+            E.fit = w.fit;
+            E.n_dev = w.count;
             ch.w = w;
             ch.E = E;
         }
@@ -1368,22 +1378,15 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                 for (size_t k = 0; k < chains.size(); ++k) {
                     const Group& G = groups[k];
                     const Chain& ch = chains[k];
-                    const int ni = G.i1 - G.i0;
                     auto b = [&] {
-                        if (G.cell)
-                            CK(launch_breed(I->d, cdev + G.i0, ni, G.units, nullptr, 0, 0, ch.w, ch.st));
-                        else
-                            CK(launch_breed(I->d, nullptr, 0, 0, pdev + G.i0, ni, G.units, ch.w, ch.st));
+                        CK(launch_breed(I->d, cdev + G.c0, G.c1 - G.c0, G.cells, pdev + G.p0, G.p1 - G.p0, G.pairs,
+                                        ch.w, ch.st));
                     };
                     auto e = [&] {
-                        CK(launch_eval(I->d, I->ec_step, ch.E, G.cell ? G.units : 2 * G.units, I->sm_count, false,
-                                       ch.st));
+                        CK(launch_eval(I->d, I->ec_step, ch.E, G.cells + 2 * G.pairs, I->sm_count, false, ch.st));
                     };
                     auto c = [&] {
-                        if (G.cell)
-                            CK(launch_commit(I->d, cdev + G.i0, ni, nullptr, 0, ch.w, ch.st));
-                        else
-                            CK(launch_commit(I->d, nullptr, 0, pdev + G.i0, ni, ch.w, ch.st));
+                        CK(launch_commit(I->d, cdev + G.c0, G.c1 - G.c0, pdev + G.p0, G.p1 - G.p0, ch.w, ch.st));
                     };
                     if (timed) {
                         I->timed_on(1, ch.st, b);
@@ -1401,7 +1404,8 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                 CK(cudaStreamWaitEvent(I->stream, I->side_join[k - 1], 0));
             }
         };
-        const long long per_gen = 4 * (long long)groups.size();
+        long long per_gen = 0;
+        for (const Group& G : groups) per_gen += 3 + (G.cells ? 1 : 0) + (G.pairs ? 1 : 0);
         // graphs pay off when a generation is launch bound (small islands); capturing costs
         // ~0.1 s, so large work lists run plain launches
         const bool use_graph = !I->timing && generations >= 2 && cap <= 16384 && !std::getenv("FFSGA_NO_GRAPH");

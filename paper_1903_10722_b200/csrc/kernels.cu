@@ -954,6 +954,7 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
     __syncwarp();
 
     // mutation (cellular.cpp:148-150)
+    const double invS = 1.0 / (double)I.S;
     const unsigned long long thr = C.thr_mu;
     const bool always = thr >= (1ull << 53);                  // p = 1: every coin is true
     const unsigned long long ulim = always ? 0ull : (thr << 11);  // (u>>11) < thr  <=>  u < thr<<11
@@ -969,17 +970,24 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
             const unsigned long long u = draw(cs, p0 + t);
             tb |= ((always || u < ulim) ? 1u : 0u) << t;
         }
-        // which draws of this lane's slice are coins, for both entry states
-        unsigned cm1 = 0, cm0 = 0;
-        int f1 = 1, f0 = 0;
-#pragma unroll
-        for (int t = 0; t < kMutChunk; ++t) {
-            const int bit = (tb >> t) & 1;
-            cm1 |= (unsigned)f1 << t;
-            cm0 |= (unsigned)f0 << t;
-            f1 = f1 ? !bit : 1;
-            f0 = f0 ? !bit : 1;
-        }
+        // which draws of this lane's slice are coins, for both entry states.  A true coin makes
+        // the next draw an index draw, which cannot itself start another -- the escape rule of
+        // backslashes in a string -- so the index (escaped) positions follow bit-parallel from
+        // the carry trick for runs of escapes (add on odd run starts, flip every other bit).
+        static_assert(kMutChunk == 16, "the escape masks below are written for 16-draw slices");
+        auto coins = [tb](unsigned first_is_index, unsigned& cm, int& next_is_coin) {
+            const unsigned bs = tb & ~first_is_index;                    // an index draw escapes nothing
+            const unsigned follows = (bs << 1) | first_is_index;
+            const unsigned odd_starts = bs & ~0x5555u & ~follows;
+            const unsigned flip = (odd_starts + bs) << 1;
+            const unsigned esc = (0x5555u ^ flip) & follows & 0xFFFFu;    // index draws
+            cm = ~esc & 0xFFFFu;
+            next_is_coin = ((cm & tb) >> 15) & 1u ? 0 : 1;
+        };
+        unsigned cm1, cm0;
+        int f1, f0;
+        coins(0u, cm1, f1);
+        coins(1u, cm0, f0);
         const int c1 = __popc(cm1), c0 = __popc(cm0);
         // inclusive scan (composition) over lanes
         int F0 = f0, F1 = f1, C0 = c0, C1 = c1;
@@ -1022,7 +1030,10 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
             im &= im - 1u;
             const int gene = g + __popc(cm & ((1u << t) - 1u)) - 1;
             if (gene < L) {
-                const int j = gene / I.S, s = gene - j * I.S;
+                int j = (int)((double)gene * invS);  // gene / S without an integer divide
+                j -= (j * I.S > gene) ? 1 : 0;
+                j += ((j + 1) * I.S <= gene) ? 1 : 0;
+                const int s = gene - j * I.S;
                 child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(draw(cs, p0 + t), __ldg(I.M + s));
             }
         }

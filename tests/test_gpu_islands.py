@@ -109,10 +109,11 @@ def test_pseudo_steps_match_oracle(capi, orc, J, S, lo, hi, n, xr):
         assert tp[0, 0] == op.archive()[2]
 
 
-@pytest.mark.parametrize("split", ["1", "2", "3"])
-def test_joint_step_equals_separate(capi, orc, monkeypatch, split):
-    # step groups (one stream per group of islands) must not change any result
+@pytest.mark.parametrize("split,mix", [("1", "0"), ("2", "0"), ("3", "0"), ("1", "1"), ("1", "2"), ("1", "3")])
+def test_joint_step_equals_separate(capi, orc, monkeypatch, split, mix):
+    # step groups (one stream per group of islands, one or both kinds per group) change no result
     monkeypatch.setenv("FFSGA_STEP_SPLIT", split)  # read when the instance is created
+    monkeypatch.setenv("FFSGA_STEP_MIX", mix)
     d = synthetic(orc, 40, 6, 2, 6)
     oi = orc.instance(d)
     emax = oi.estimate_emax()
