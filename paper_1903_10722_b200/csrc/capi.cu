@@ -484,7 +484,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         CK(cudaEventCreate(&I->st1));
         I->wl_count.alloc(2 * sizeof(long long));  // one item counter per joint-step group (grown on demand)
         I->eval_total.alloc(sizeof(unsigned long long));
-        CK(cudaMemset(I->eval_total.p, 0, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(I->eval_total.p, 0, sizeof(unsigned long long), I->stream));
         *out = hold.release();
     });
 }
@@ -631,7 +631,7 @@ int ffsga_cuda_batch_create(ffsga_cuda_instance inst, int64_t capacity, ffsga_cu
         b->mk.alloc(sizeof(double) * capacity);
         b->td.alloc(sizeof(double) * capacity);
         b->err.alloc(sizeof(unsigned long long));
-        CK(cudaMemset(b->err.p, 0xFF, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(b->err.p, 0xFF, sizeof(unsigned long long), inst->stream));
         CK(cudaEventCreate(&b->e0));
         CK(cudaEventCreate(&b->e1));
         *out = hold.release();
@@ -707,7 +707,7 @@ int ffsga_cuda_batch_results(ffsga_cuda_batch b, int64_t n, double* obj, double*
         CK(cudaMemcpyAsync(&code, b->err.p, sizeof(code), cudaMemcpyDeviceToHost, I->stream));
         CK(cudaStreamSynchronize(I->stream));
         if (code != kNoError) {
-            CK(cudaMemset(b->err.p, 0xFF, sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(b->err.p, 0xFF, sizeof(unsigned long long), I->stream));
             fail(FFSGA_ERR_CONTRACT, gene_error(code) + " (chromosome " + std::to_string(code >> 32) + ")");
         }
     });
@@ -761,7 +761,8 @@ struct ffsga_cuda_cellular_t {
     void push_desc() {
         d.trace = trace.as<double>();
         desc.ensure(sizeof(CellIsland));
-        CK(cudaMemcpy(desc.p, &d, sizeof(CellIsland), cudaMemcpyHostToDevice));
+        // stream-ordered after any kernel that still reads the old descriptor (pageable: staged)
+        CK(cudaMemcpyAsync(desc.p, &d, sizeof(CellIsland), cudaMemcpyHostToDevice, inst->stream));
     }
 };
 
@@ -775,7 +776,7 @@ struct ffsga_cuda_pseudo_t {
     void push_desc() {
         d.trace = trace.as<double>();
         desc.ensure(sizeof(PseudoIsland));
-        CK(cudaMemcpy(desc.p, &d, sizeof(PseudoIsland), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(desc.p, &d, sizeof(PseudoIsland), cudaMemcpyHostToDevice, inst->stream));
     }
 };
 
@@ -859,13 +860,13 @@ int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, 
         const size_t block = I->block();
         c->genes.alloc(2 * (size_t)c->n * block);  // slot 1 is written by the first breed, pads included
         c->sel.alloc(2 * (size_t)c->n);
-        CK(cudaMemset(c->sel.p, 0, 2 * (size_t)c->n));
+        CK(cudaMemsetAsync(c->sel.p, 0, 2 * (size_t)c->n, I->stream));
         c->fit.alloc(2 * sizeof(double) * c->n);
         c->obj.alloc(2 * sizeof(double) * c->n);
         c->st.alloc(sizeof(IslandState));
         IslandState s0{};
         s0.arch_fit = -1.0;
-        CK(cudaMemcpy(c->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(c->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice, I->stream));  // pageable: staged
         c->trace_cap = 1;
         c->trace.alloc(sizeof(double));
         if (init_genes) {
@@ -881,9 +882,14 @@ int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, 
             CK(launch_random_rows(I->d, c->genes.as<uint8_t>(), (long long)block, c->n, seed, 0, false, I->stream));
             g_launches += 1;
         }
-        eval_rows(I, c->genes.as<uint8_t>(), c->n, c->obj.as<double>(), c->fit.as<double>(), nullptr, nullptr, true);
-        const unsigned long long code = read_error(I);
-        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        // device-generated genes are in range by construction: only explicit populations are
+        // checked (and only then does creation wait for the device)
+        eval_rows(I, c->genes.as<uint8_t>(), c->n, c->obj.as<double>(), c->fit.as<double>(), nullptr, nullptr,
+                  init_genes != nullptr);
+        if (init_genes) {
+            const unsigned long long code = read_error(I);
+            if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+        }
         CellIsland& d = c->d;
         d.n = c->n;
         d.width = width;
@@ -902,8 +908,7 @@ int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, 
         d.cell0 = 0;
         c->push_desc();
         refresh_stats(c, nullptr, 0);
-        CK(cudaStreamSynchronize(I->stream));
-        *out = hold.release();
+        *out = hold.release();  // stream-ordered: every later call on the instance sees the initial state
     });
 }
 
@@ -1075,12 +1080,12 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         p->obj.alloc(sizeof(double) * population);
         p->mslot.alloc(sizeof(long long) * population);
         p->archive.alloc(sizeof(unsigned long long) * W);
-        CK(cudaMemset(p->archive.p, 0, sizeof(unsigned long long) * W));
+        CK(cudaMemsetAsync(p->archive.p, 0, sizeof(unsigned long long) * W, I->stream));
         p->st.alloc(sizeof(IslandState));
         IslandState s0{};
         s0.arch_fit = -1.0;  // pseudo.hpp:79
         s0.arch_obj = 0.0;
-        CK(cudaMemcpy(p->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(p->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice, I->stream));  // pageable: staged
         p->trace_cap = 1;
         p->trace.alloc(sizeof(double));
         // pairs (x, ~x): x = pair p's chromosome of the sequential init stream (pseudo.cpp:40-47)
@@ -1093,10 +1098,8 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         CK(launch_unpack_rows(I->d, p->words.as<unsigned long long>(), nullptr, rows, (long long)block, nullptr,
                               population, I->stream));
         g_launches += 3;
-        eval_rows(I, rows, population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, true);
-        const unsigned long long code = read_error(I);
-        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
-        PseudoIsland& d = p->d;
+        eval_rows(I, rows, population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, false);
+        PseudoIsland& d = p->d;  // (device-generated genes: in range by construction)
         d.n = population;
         d.words = p->words.as<unsigned long long>();
         d.fit = p->fit.as<double>();
@@ -1109,8 +1112,7 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         d.pair0 = 0;
         p->push_desc();
         refresh_stats(nullptr, p, 2);  // archive = first max over the scored members
-        CK(cudaStreamSynchronize(I->stream));
-        *out = hold.release();
+        *out = hold.release();          // stream-ordered, as cellular_create
     });
 }
 
