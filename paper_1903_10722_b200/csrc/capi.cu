@@ -71,14 +71,22 @@ inline void pool_setup_once() {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    // Stream on which every use of the buffer is ordered (island and batch buffers: the instance
+    // stream).  Such a buffer is freed stream-ordered, without blocking the host or other
+    // instances' work; an unowned buffer keeps cudaFree's device-wide synchronisation.
+    cudaStream_t owner = nullptr;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
         if (p) {
-            cudaDeviceSynchronize();  // every use of the buffer has completed (cudaFree semantics)
-            cudaFreeAsync(p, 0);
+            if (owner) {
+                cudaFreeAsync(p, owner);
+            } else {
+                cudaDeviceSynchronize();  // every use of the buffer has completed (cudaFree semantics)
+                cudaFreeAsync(p, 0);
+            }
         }
         p = nullptr;
         bytes = 0;
@@ -582,6 +590,9 @@ struct ffsga_cuda_batch_t {
     ffsga_cuda_instance_t* inst = nullptr;
     long long cap = 0;
     DevBuf rows, obj, fit, mk, td, err, stage;
+    void adopt(cudaStream_t s) {
+        for (DevBuf* b : {&rows, &obj, &fit, &mk, &td, &err, &stage}) b->owner = s;
+    }
     long long stage_cap = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     ~ffsga_cuda_batch_t() {
@@ -624,6 +635,7 @@ int ffsga_cuda_batch_create(ffsga_cuda_instance inst, int64_t capacity, ffsga_cu
         auto* b = new ffsga_cuda_batch_t();
         std::unique_ptr<ffsga_cuda_batch_t> hold(b);
         b->inst = inst;
+        b->adopt(inst->stream);
         b->cap = capacity;
         b->rows.alloc((size_t)capacity * inst->block());
         b->obj.alloc(sizeof(double) * capacity);
@@ -757,6 +769,9 @@ struct ffsga_cuda_cellular_t {
     DevBuf genes, sel, fit, obj, slots, st, trace, desc;
     long long trace_cap = 0;
     CellIsland d{};
+    void adopt(cudaStream_t s) {
+        for (DevBuf* b : {&genes, &sel, &fit, &obj, &slots, &st, &trace, &desc}) b->owner = s;
+    }
     int parity() const { return (int)(gen & 1ull); }
     void push_desc() {
         d.trace = trace.as<double>();
@@ -773,6 +788,9 @@ struct ffsga_cuda_pseudo_t {
     DevBuf words, fit, obj, mslot, archive, st, trace, desc;
     long long trace_cap = 0;
     PseudoIsland d{};
+    void adopt(cudaStream_t s) {
+        for (DevBuf* b : {&words, &fit, &obj, &mslot, &archive, &st, &trace, &desc}) b->owner = s;
+    }
     void push_desc() {
         d.trace = trace.as<double>();
         desc.ensure(sizeof(PseudoIsland));
@@ -850,6 +868,7 @@ int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, 
         auto* c = new ffsga_cuda_cellular_t();
         std::unique_ptr<ffsga_cuda_cellular_t> hold(c);
         c->inst = I;
+        c->adopt(I->stream);
         c->W = width;
         c->H = height;
         c->n = width * height;
@@ -1073,6 +1092,7 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         auto* p = new ffsga_cuda_pseudo_t();
         std::unique_ptr<ffsga_cuda_pseudo_t> hold(p);
         p->inst = I;
+        p->adopt(I->stream);
         p->n = population;
         const int W = I->words;
         p->words.alloc(sizeof(unsigned long long) * (size_t)W * population);
