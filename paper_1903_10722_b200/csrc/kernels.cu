@@ -1385,11 +1385,15 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
 }  // namespace
 
 int eval_config(const DevInst& I, int sm_count, int warps_cap, bool early, EvalConfig* cfg) {
-    if (I.maxM <= 4) return eval_config_g<4>(I, sm_count, warps_cap, early, cfg);
-    if (I.maxM <= 8) return eval_config_g<8>(I, sm_count, warps_cap, early, cfg);
-    if (I.maxM <= 16) return eval_config_g<16>(I, sm_count, warps_cap, early, cfg);
+    // The smallest group that covers the widest stage; when a warp of such groups does not fit
+    // shared memory (large J), wider groups put fewer chromosomes in a warp (idle lanes) so that
+    // one chromosome may use up to a whole CTA's shared memory.
+    int rc = -3;
+    if (I.maxM <= 4 && (rc = eval_config_g<4>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
+    if (I.maxM <= 8 && (rc = eval_config_g<8>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
+    if (I.maxM <= 16 && (rc = eval_config_g<16>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
     if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, warps_cap, early, cfg);
-    return -3;
+    return rc;
 }
 
 cudaError_t launch_eval(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,

@@ -226,3 +226,25 @@ def test_sub_ulp_processing_times(capi, orc):
     eo, ef, em, et = oi.score_batch(pop, emax)
     for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("J,S,lo,hi", [(4000, 3, 2, 2), (9000, 2, 2, 3), (20000, 2, 2, 2)])
+def test_large_jobs_wider_groups(capi, orc, J, S, lo, hi):
+    """Per-chromosome state grows with J: past a warp of minimal groups the decoder switches to
+    wider groups (fewer chromosomes per warp) instead of refusing the instance."""
+    d = synthetic(orc, J, S, lo, hi)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    assert inst.info()["group_lanes"] > 4
+    pop = oi.random_population(5, 0, 12)
+    obj, fit, mk, td = inst.evaluate(pop, full=True)
+    eo, ef, em, et = oi.score_batch(pop, emax)
+    for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_too_many_jobs_is_a_config_error(capi, orc):
+    d = synthetic(orc, 30000, 2, 2, 2)
+    with pytest.raises(capi.ConfigError, match="too large"):
+        capi.Instance.from_data(d, 1e12)
