@@ -15,6 +15,7 @@
 #include <cuda_pipeline.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "launch.h"
@@ -923,38 +924,57 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
     const uint8_t* g1 = C.genes + ((size_t)selq[p1] * n + p1) * block;
     const uint8_t* g2 = C.genes + ((size_t)selq[p2] * n + p2) * block;
 
-    // two-point crossover on the job-major index i = j*S + s (cellular.cpp:136-146)
+    // two-point crossover on the job-major index i = j*S + s (cellular.cpp:136-146): in stage
+    // row s, jobs j with lo <= j*S+s < hi, i.e. ceil((lo-s)/S) <= j < ceil((hi-s)/S), take parent 2
     const int vec_per_row = I.Jpad / 16;
-    for (int v = lane; v < I.S * vec_per_row; v += 32) {
-        const int s = v / vec_per_row;
-        const int j0 = (v % vec_per_row) * 16;
-        uint4 a = __ldg(reinterpret_cast<const uint4*>(g1 + (size_t)s * I.Jpad) + (j0 / 16));
+    const double invS = 1.0 / (double)I.S;
+    auto ceil_div_S = [&](int x) {  // ceil(x / S) for x >= 0, divide-free
+        int q = (int)((double)x * invS);
+        q -= (q * I.S > x) ? 1 : 0;
+        q += ((q + 1) * I.S <= x) ? 1 : 0;  // q = floor(x / S)
+        return q + ((q * I.S < x) ? 1 : 0);
+    };
+    auto byte_mask = [](int b0, int b1, int w) {  // bytes [b0, b1) of word w (bytes 4w..4w+3)
+        const int l = min(max(b0 - 4 * w, 0), 4), h = min(max(b1 - 4 * w, 0), 4);
+        const unsigned ml = l >= 4 ? 0u : (0xFFFFFFFFu << (8 * l));
+        const unsigned mh = h >= 4 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu << (8 * h));
+        return ml & mh;
+    };
+    int s = 0, vr = lane;  // vector lane of stage row s, stepping by 32 without a divide
+    while (vr >= vec_per_row && s < I.S) {
+        vr -= vec_per_row;
+        ++s;
+    }
+    for (; s < I.S;) {
+        const int j0 = vr * 16;
+        uint4 a = __ldg(reinterpret_cast<const uint4*>(g1 + (size_t)s * I.Jpad) + vr);
         if (crossed) {
-            // jobs with lo <= j*S+s < hi take parent 2
-            const int jlo = lo - s <= 0 ? 0 : (lo - s + I.S - 1) / I.S;
-            const int jhi = hi - s <= 0 ? 0 : (hi - s + I.S - 1) / I.S;
+            const int jlo = lo - s <= 0 ? 0 : ceil_div_S(lo - s);
+            const int jhi = hi - s <= 0 ? 0 : ceil_div_S(hi - s);
             if (jlo < j0 + 16 && jhi > j0 && jlo < jhi) {
-                const uint4 b = __ldg(reinterpret_cast<const uint4*>(g2 + (size_t)s * I.Jpad) + (j0 / 16));
-                unsigned* pa = reinterpret_cast<unsigned*>(&a);
-                const unsigned* pb = reinterpret_cast<const unsigned*>(&b);
-#pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    unsigned msk = 0;
-#pragma unroll
-                    for (int by = 0; by < 4; ++by) {
-                        const int j = j0 + 4 * w + by;
-                        if (j >= jlo && j < jhi) msk |= 0xFFu << (8 * by);
-                    }
-                    pa[w] = (pa[w] & ~msk) | (pb[w] & msk);
-                }
+                const uint4 b = __ldg(reinterpret_cast<const uint4*>(g2 + (size_t)s * I.Jpad) + vr);
+                const int b0 = jlo - j0, b1 = jhi - j0;
+                unsigned m;
+                m = byte_mask(b0, b1, 0);
+                a.x = (a.x & ~m) | (b.x & m);
+                m = byte_mask(b0, b1, 1);
+                a.y = (a.y & ~m) | (b.y & m);
+                m = byte_mask(b0, b1, 2);
+                a.z = (a.z & ~m) | (b.z & m);
+                m = byte_mask(b0, b1, 3);
+                a.w = (a.w & ~m) | (b.w & m);
             }
         }
-        reinterpret_cast<uint4*>(child + (size_t)s * I.Jpad)[j0 / 16] = a;
+        reinterpret_cast<uint4*>(child + (size_t)s * I.Jpad)[vr] = a;
+        vr += 32;
+        while (vr >= vec_per_row && s < I.S) {
+            vr -= vec_per_row;
+            ++s;
+        }
     }
     __syncwarp();
 
     // mutation (cellular.cpp:148-150)
-    const double invS = 1.0 / (double)I.S;
     const unsigned long long thr = C.thr_mu;
     const bool always = thr >= (1ull << 53);                  // p = 1: every coin is true
     const unsigned long long ulim = always ? 0ull : (thr << 11);  // (u>>11) < thr  <=>  u < thr<<11
@@ -1356,6 +1376,7 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, bool early, Eva
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, 32 * warps, cfg->smem);
     if (e != cudaSuccess || occ < 1) return -2;
+    if (const char* v = getenv("FFSGA_EVAL_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(v)));  // experiments
     cfg->blocks_per_sm = occ;
     return 0;
 }
