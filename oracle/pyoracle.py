@@ -542,6 +542,10 @@ class RefLib:
         L.ref_run_migration.argtypes = [_vp, _i32, _pu64, _pd, _pd, _pi, _pi]
         L.ref_run_traces.argtypes = [_vp, _pd, _pd, _pd, _pi]
         L.ref_run_free.argtypes = [_vp]
+        for f in ("ref_save_result_json", "ref_save_trace_csv", "ref_save_instance"):
+            if hasattr(L, f):  # io.cpp (file formats); absent from older builds
+                getattr(L, f).restype = _i32
+                getattr(L, f).argtypes = [_vp, C.c_char_p]
 
     def generate(self, jobs, stages, machines, weight=100.0, seed=1, integer_times=False):
         m = np.ascontiguousarray(machines, dtype=np.int32)
@@ -622,14 +626,23 @@ class RefInstance:
             raise ValueError(self.lib.ref_last_error().decode())
         return RefPseudo(self, h)
 
+    def save(self, path):
+        """ffsga::save_instance (io.cpp) -- the reference's instance JSON bytes."""
+        if self.lib.ref_save_instance(self.h, str(path).encode()) != 0:
+            raise OSError(self.lib.ref_last_error().decode())
+
     def run(self, population=512, generations=2000, gap=500, theta=1.0, mode="dual", seed=1,
             workers=1, serialized=False, cellular_crossover=1.0, cellular_mutation=0.05,
-            pseudo_crossover=0.75, pseudo_fit_from_archive=False):
+            pseudo_crossover=0.75, pseudo_fit_from_archive=False, result_json=None, trace_csv=None):
         r = self.lib.ref_run(self.h, population, generations, gap, theta, MODES[mode], _u64(seed),
                              workers, int(serialized), cellular_crossover, cellular_mutation,
                              pseudo_crossover, int(pseudo_fit_from_archive))
         if not r:
             raise ValueError(self.lib.ref_last_error().decode())
+        if result_json is not None:  # ffsga::save_result_json / save_trace_csv (io.cpp)
+            self.lib.ref_save_result_json(r, str(result_json).encode())
+        if trace_csv is not None:
+            self.lib.ref_save_trace_csv(r, str(trace_csv).encode())
         sc = np.empty(5)
         self.lib.ref_run_scalars(r, _ptr(sc, _pd))
         G, L = generations, self.data.num_genes

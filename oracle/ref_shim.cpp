@@ -14,6 +14,7 @@
 #include "ffsga/cellular.hpp"
 #include "ffsga/chromosome.hpp"
 #include "ffsga/generator.hpp"
+#include "ffsga/io.hpp"
 #include "ffsga/migration.hpp"
 #include "ffsga/model.hpp"
 #include "ffsga/parallel.hpp"
@@ -291,6 +292,7 @@ void ref_migrate_p2c(void* p, void* g, int k) {
 // ---- whole run --------------------------------------------------------------------------
 struct RefRun {
     RunResult r;
+    RunConfig c;
 };
 
 void* ref_run(void* h, int population, int generations, int gap, double theta, int mode,
@@ -311,6 +313,7 @@ void* ref_run(void* h, int population, int generations, int gap, double theta, i
         c.pseudo.crossover_rate = px;
         c.pseudo_fit_from_archive = pseudo_fit_from_archive != 0;
         auto* rr = new RefRun();
+        rr->c = c;
         rr->r = serialized ? run_serialized(c, *static_cast<Instance*>(h)) : run(c, *static_cast<Instance*>(h));
         out = rr;
     });
@@ -342,5 +345,16 @@ void ref_run_traces(void* r, double* combined, double* a, double* b, int32_t* ch
     std::memcpy(chromosome, x.best_chromosome.genes.data(), sizeof(int) * x.best_chromosome.genes.size());
 }
 void ref_run_free(void* r) { delete static_cast<RefRun*>(r); }
+
+// ---- file formats (io.cpp): result JSON, trace CSV, instance JSON ------------------------
+int ref_save_result_json(void* r, const char* path) {
+    return guard([&] { save_result_json(static_cast<RefRun*>(r)->r, static_cast<RefRun*>(r)->c, path); });
+}
+int ref_save_trace_csv(void* r, const char* path) {
+    return guard([&] { save_trace_csv(static_cast<RefRun*>(r)->r, path); });
+}
+int ref_save_instance(void* h, const char* path) {
+    return guard([&] { save_instance(*static_cast<Instance*>(h), path); });
+}
 
 }  // extern "C"

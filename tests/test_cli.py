@@ -165,3 +165,46 @@ def test_compare_sweep_and_bench_tables(tmp_path):
     rows = lines_of(out)
     assert rows[0] == "population,concurrent_seconds,serialized_seconds,speedup"
     assert rows[1].startswith("8,") and rows[2].startswith("16,")
+
+
+def _doc_without_timings(text):
+    from collections import OrderedDict
+    doc = json.loads(text, parse_float=str, object_pairs_hook=OrderedDict)  # numbers keep their text
+    doc.pop("timings", None)
+    return doc
+
+
+def test_instance_file_bytes_match_reference(tmp_path, ref):
+    """`generate` writes the reference's instance JSON byte for byte (io.cpp save_instance)."""
+    import numpy as np
+    from pyoracle import InstanceData
+    ours = tmp_path / "ours.json"
+    assert run_cli("generate", "--jobs", 30, "--stages", 4, "--machines", "2,3,1,4", "--seed", 11, "--wt", 7.5,
+                   "--out", ours)[0] == 0
+    d = ref.generate(30, 4, [2, 3, 1, 4], weight=7.5, seed=11)
+    theirs = tmp_path / "theirs.json"
+    ref.instance(d).save(theirs)
+    assert ours.read_bytes() == theirs.read_bytes()
+
+
+@pytest.mark.gpu
+def test_result_and_trace_files_match_reference(tmp_path, ref):
+    """`solve` writes the reference's result JSON (outside `timings`) and trace CSV byte for byte
+    (io.cpp save_result_json / save_trace_csv), migrations included."""
+    import numpy as np
+    from pyoracle import InstanceData
+    for seed in (4, 12):  # tests/golden: runs with migrations at these seeds
+        inst = tmp_path / f"in{seed}.json"
+        assert run_cli("generate", "--jobs", 8, "--stages", 2, "--machines", 2, "--wt", 0, "--seed", seed,
+                       "--out", inst)[0] == 0
+        ours, ours_tr = tmp_path / f"ours{seed}.json", tmp_path / f"ours{seed}.csv"
+        code, _, err = run_cli("solve", "--instance", inst, "--population", 64, "--generations", 30, "--gap", 1,
+                               "--seed", seed, "--out", ours, "--trace", ours_tr)
+        assert code == 0, err
+        d = ref.generate(8, 2, [2, 2], weight=0.0, seed=seed)
+        theirs, theirs_tr = tmp_path / f"theirs{seed}.json", tmp_path / f"theirs{seed}.csv"
+        r = ref.instance(d).run(population=64, generations=30, gap=1, seed=seed, result_json=theirs,
+                                trace_csv=theirs_tr)
+        assert r["migrations"], "the fixture seeds fire migrations"
+        assert _doc_without_timings(ours.read_text()) == _doc_without_timings(theirs.read_text())
+        assert ours_tr.read_bytes() == theirs_tr.read_bytes()
