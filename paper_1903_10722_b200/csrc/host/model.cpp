@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -151,6 +152,21 @@ std::uint64_t digest(const Instance& inst, double emax) {
 
 std::mutex g_registry_mu;
 std::multimap<std::uint64_t, Entry> g_registry;
+// The reference API evaluates through free functions (decode, Evaluator on a stack instance) in
+// tight loops: the most recently used device instances stay alive so such a loop pays the
+// device upload once, not per call.  Never destroyed (process exit releases the device).
+constexpr size_t kRecent = 4;
+std::deque<std::shared_ptr<DeviceInstance>>* g_recent = new std::deque<std::shared_ptr<DeviceInstance>>();
+
+void touch(const std::shared_ptr<DeviceInstance>& dev) {
+    for (auto it = g_recent->begin(); it != g_recent->end(); ++it)
+        if (*it == dev) {
+            g_recent->erase(it);
+            break;
+        }
+    g_recent->push_front(dev);
+    if (g_recent->size() > kRecent) g_recent->pop_back();
+}
 
 }  // namespace
 
@@ -176,7 +192,10 @@ std::shared_ptr<DeviceInstance> DeviceInstance::get(const Instance& inst, double
     auto range = g_registry.equal_range(key);
     for (auto it = range.first; it != range.second;) {
         if (auto dev = it->second.dev.lock()) {
-            if (it->second.emax == emax && same(it->second.copy, inst)) return dev;
+            if (it->second.emax == emax && same(it->second.copy, inst)) {
+                touch(dev);
+                return dev;
+            }
             ++it;
         } else {
             it = g_registry.erase(it);
@@ -184,6 +203,7 @@ std::shared_ptr<DeviceInstance> DeviceInstance::get(const Instance& inst, double
     }
     auto dev = std::make_shared<DeviceInstance>(inst, emax);
     g_registry.emplace(key, Entry{inst, emax, dev});
+    touch(dev);
     return dev;
 }
 
