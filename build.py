@@ -114,7 +114,7 @@ def build_cli(force=False):
 
 
 def build_oracle(force=False):
-    args = ["make", "-s", "-f", os.path.join(ROOT, "oracle", "Makefile"), "all", "acceptance"]
+    args = ["make", "-s", "-f", os.path.join(ROOT, "oracle", "Makefile"), "all", "acceptance", "unit"]
     if force:
         args.append("-B")
     _run(args)

@@ -38,3 +38,15 @@ def test_whole_run_means_bit_identical(gate_output):
     assert "dual 3561.57051120799, cellular 3561.57051120799, pseudo 3771.4406734010736" in out
     assert "evaluator matched the exhaustive reference on 20/20 instances" in out
     assert "result documents outside timings byte-identical" in out and "traces byte-identical" in out
+
+
+def test_reference_unit_suite_on_our_library():
+    """The reference's doctest unit suite (proj/tests/test_*.cpp: 102 test cases), unmodified,
+    compiled against this repo's headers with oracle/doctest_shim standing in for doctest, linked
+    to the B200 library, CLI cases driving bin/ffsga."""
+    unit = os.path.join(ROOT, "oracle", "_ref", "unit_b200")
+    if not os.path.exists(unit):
+        pytest.skip("oracle/_ref/unit_b200 not built (needs the reference sources at build time)")
+    p = subprocess.run([unit], capture_output=True, text=True, timeout=1200, env=dict(os.environ, FFSGA_CLI=CLI))
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert "test cases: 102 | 102 passed | 0 failed" in p.stdout
