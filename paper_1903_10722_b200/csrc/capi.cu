@@ -1412,7 +1412,9 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                                         ch.w, ch.st));
                     };
                     auto e = [&] {
-                        CK(launch_eval(I->d, I->ec_step, ch.E, G.cells + 2 * G.pairs, I->sm_count, false, ch.st));
+                        // one group alone owns the GPU: the standalone configuration fits it best
+                        const EvalConfig& ec = groups.size() == 1 ? I->ec : I->ec_step;
+                        CK(launch_eval(I->d, ec, ch.E, G.cells + 2 * G.pairs, I->sm_count, false, ch.st));
                     };
                     auto c = [&] {
                         CK(launch_commit(I->d, cdev + G.c0, G.c1 - G.c0, pdev + G.p0, G.p1 - G.p0, ch.w, ch.st));
