@@ -77,6 +77,13 @@ int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t 
 /* Same with one byte per gene (the compact host layout of the e2e decoder benchmark). */
 int ffsga_cuda_evaluate_u8(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* objective,
                            double* fitness, double* makespan, double* tardiness);
+/* Same for a population already resident in device memory (torch / DLPack
+ * tensors): genes, objective, fitness (and the optional makespan / tardiness) are DEVICE pointers
+ * of the instance's device, genes job-major one byte per gene.  The work is ordered after
+ * everything already queued on `stream` (a cudaStream_t; NULL = legacy default stream) and
+ * everything queued on it afterwards sees the results.  Out-of-range genes fail as above. */
+int ffsga_cuda_evaluate_device(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* objective,
+                               double* fitness, double* makespan, double* tardiness, void* stream);
 
 /* ---- K7: schedule materialization ----------------------------------------------------------
  * Replaces: Schedule decode(const Instance&, span<const int>) (model.hpp:42, model.cpp:124-139)

@@ -50,6 +50,7 @@ _SIGS = {
     "ffsga_cuda_instance_info": (_i32, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "ffsga_cuda_evaluate": (_i32, [_vp, _pi32, _i64, _pd, _pd, _pd, _pd]),
     "ffsga_cuda_evaluate_u8": (_i32, [_vp, _pu8, _i64, _pd, _pd, _pd, _pd]),
+    "ffsga_cuda_evaluate_device": (_i32, [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "ffsga_cuda_decode": (_i32, [_vp, _pi32, _pi32, _pd, _pd, _pd]),
     "ffsga_cuda_batch_create": (_i32, [_vp, _i64, _pvp]),
     "ffsga_cuda_batch_destroy": (_i32, [_vp]),
@@ -201,6 +202,13 @@ class Instance:
         td = np.empty(n) if full else None
         _check(fn(self.h, gp, n, _p(obj, _pd), _p(fit, _pd), _p(mk, _pd), _p(td, _pd)))
         return (obj, fit, mk, td) if full else (obj, fit)
+
+    def evaluate_device(self, genes_ptr, n, obj_ptr, fit_ptr, mk_ptr=None, td_ptr=None, stream=None):
+        """Evaluator::score over n device-resident job-major u8 chromosomes; every argument is a
+        raw device pointer (int), results land in device memory, ordered on `stream`."""
+        _check(lib().ffsga_cuda_evaluate_device(self.h, C.c_void_p(genes_ptr), n, C.c_void_p(obj_ptr),
+                                                C.c_void_p(fit_ptr), C.c_void_p(mk_ptr or 0), C.c_void_p(td_ptr or 0),
+                                                C.c_void_p(stream or 0)))
 
     def decode(self, genes):
         """decode + evaluate of one chromosome -> (machine, start, completion, report dict)."""

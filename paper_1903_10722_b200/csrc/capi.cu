@@ -529,6 +529,38 @@ int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t 
     });
 }
 
+int ffsga_cuda_evaluate_device(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* obj, double* fit,
+                               double* mk, double* td, void* stream) {
+    return guard([&] {
+        if (!inst) fail(FFSGA_ERR_ARG, "null instance");
+        if (n < 0) fail(FFSGA_ERR_CONTRACT, "evaluate: negative batch size");
+        if (n == 0) return;
+        if (!genes || !obj || !fit) fail(FFSGA_ERR_ARG, "evaluate: null pointer");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        ffsga_cuda_instance_t* I = inst;
+        cudaStream_t user = static_cast<cudaStream_t>(stream);
+        // order: caller's queued work -> our stream -> back to the caller's stream
+        CK(cudaEventRecord(I->fork, user));
+        CK(cudaStreamWaitEvent(I->stream, I->fork, 0));
+        const long long L = (long long)I->J * I->S;
+        const long long chunk = std::min<long long>(n, 1 << 16);
+        ensure_eval_staging(I, chunk);
+        for (long long first = 0; first < n; first += chunk) {
+            const long long c = std::min<long long>(chunk, n - first);
+            CK(launch_rows_from_int(I->d, nullptr, genes + first * L, I->ev_rows.as<uint8_t>(), c, I->stream));
+            g_launches += 1;
+            eval_rows(I, I->ev_rows.as<uint8_t>(), c, obj + first, fit + first, mk ? mk + first : nullptr,
+                      td ? td + first : nullptr, true);
+            const unsigned long long code = read_error(I);
+            if (code != kNoError)
+                fail(FFSGA_ERR_CONTRACT, gene_error(code) + " (chromosome " + std::to_string((code >> 32) + first) + ")");
+        }
+        CK(cudaEventRecord(I->join, I->stream));
+        CK(cudaStreamWaitEvent(user, I->join, 0));
+    });
+}
+
 int ffsga_cuda_evaluate_u8(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* obj, double* fit,
                            double* mk, double* td) {
     return guard([&] {

@@ -149,3 +149,24 @@ def test_cell_candidate_matches_oracle(orc):
             eg = oc.genes()[i]
         assert np.array_equal(g, eg) and (f, o, rep) == (ef, eo, erep)
         assert used >= 4 + 1 + 12  # tournaments + coin + one coin per gene
+
+
+def test_evaluate_tensor_device_resident(orc):
+    """a population already on the GPU (torch CUDA tensor) is scored in place,
+    results stay on the device, bit-identical to the oracle; errors as the host path."""
+    import torch
+    inst = ffsga.generate_instance(jobs=100, stages=10, machines=[4, 2, 2, 3, 4, 4, 2, 3, 4, 5], seed=7)
+    oi = orc.instance(as_data(inst))
+    pop = oi.random_population(99, 0, 3000)
+    g = torch.from_numpy(pop.astype(np.uint8)).cuda()
+    obj, fit, mk, td = ffsga.evaluate_tensor(inst, g, full=True)
+    assert obj.is_cuda and obj.dtype == torch.float64
+    eo, ef, em, et = oi.score_batch(pop, oi.estimate_emax())
+    for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(a.cpu().numpy().view(np.uint64), b.view(np.uint64))
+    obj32, _ = ffsga.evaluate_tensor(inst, torch.from_numpy(pop).cuda())  # int32 input
+    assert torch.equal(obj32, obj)
+    bad = torch.from_numpy(pop[:5].copy()).cuda()
+    bad[3, 7] = 9
+    with pytest.raises(ValueError, match="out of range"):
+        ffsga.evaluate_tensor(inst, bad)
