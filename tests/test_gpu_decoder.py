@@ -248,3 +248,26 @@ def test_too_many_jobs_is_a_config_error(capi, orc):
     d = synthetic(orc, 30000, 2, 2, 2)
     with pytest.raises(capi.ConfigError, match="too large"):
         capi.Instance.from_data(d, 1e12)
+
+
+@pytest.mark.parametrize("algo", ["merge", "bucket"])
+def test_randomized_instances_both_decoders(capi, orc, monkeypatch, algo):
+    """Many random shapes (1-40 jobs... 300 jobs, 1-12 stages, 1-32 machines per stage, real and
+    integer times, random weights): both decoders bit-identical to the oracle."""
+    monkeypatch.setenv("FFSGA_EVAL_ALGO", algo)
+    rng = np.random.default_rng(20261018)
+    for case in range(24):
+        J = int(rng.choice([1, 2, 5, 17, 40, 97, 300]))
+        S = int(rng.integers(1, 13))
+        hi = int(rng.choice([2, 4, 8, 13, 32]))
+        M = [int(x) for x in rng.integers(1, hi + 1, S)]
+        d = orc.generate(J, S, M, weight=float(rng.choice([0.0, 1.0, 100.0, 7.25])), seed=int(rng.integers(1, 10**6)),
+                         integer_times=bool(rng.integers(0, 2)))
+        oi = orc.instance(d)
+        emax = oi.estimate_emax()
+        inst = capi.Instance.from_data(d, emax)
+        pop = oi.random_population(int(rng.integers(0, 10**6)), 0, 48)
+        obj, fit, mk, td = inst.evaluate(pop, full=True)
+        eo, ef, em, et = oi.score_batch(pop, emax)
+        for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (case, J, S, M)
