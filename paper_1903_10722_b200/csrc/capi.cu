@@ -4,6 +4,8 @@
 // evaluation, breeding step, replacement, archive update and migration runs in kernels.cu.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -340,6 +342,15 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
                                const double* proc, const double* release, const double* due, double weight,
                                double emax, ffsga_cuda_instance* out) {
     return guard([&] {
+        const bool dbg = std::getenv("FFSGA_DEBUG_INIT") != nullptr;
+        auto t_last = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!dbg) return;
+            const auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "instance_create %-24s %.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(t - t_last).count());
+            t_last = t;
+        };
         if (!out || !machines || !proc || !release || !due) fail(FFSGA_ERR_ARG, "instance_create: null pointer");
         *out = nullptr;
         if (num_jobs < 1) fail(FFSGA_ERR_CONTRACT, "instance: num_jobs must be >= 1");
@@ -357,10 +368,11 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         std::unique_ptr<ffsga_cuda_instance_t> hold(I);
         I->device = device;
         I->use();
-        cudaDeviceProp prop;
-        CK(cudaGetDeviceProperties(&prop, device));
-        if (prop.major < 10) fail(FFSGA_ERR_CUDA, "device is not sm_100 class (built for sm_100a only)");
-        I->sm_count = prop.multiProcessorCount;
+        // two attributes, not cudaGetDeviceProperties (which queries everything: tens of ms)
+        int cc_major = 0;
+        CK(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device));
+        if (cc_major < 10) fail(FFSGA_ERR_CUDA, "device is not sm_100 class (built for sm_100a only)");
+        CK(cudaDeviceGetAttribute(&I->sm_count, cudaDevAttrMultiProcessorCount, device));
         const int J = num_jobs, S = num_stages;
         I->J = J;
         I->S = S;
@@ -427,6 +439,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         std::vector<uint16_t> bit_stage(I->bpj);
         for (int s = 0; s < S; ++s)
             for (int r = I->sbo[s]; r < I->sbo[s + 1]; ++r) bit_stage[r] = (uint16_t)s;
+        mark("validate+layout");
         upload(I->dM, I->M);
         upload(I->dStageOff, I->stage_off);
         upload(I->dBps, I->bps);
@@ -436,6 +449,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         upload(I->dDue, std::vector<double>(due, due + J));
         upload(I->dRelOrder, order);
         upload(I->dBitStage, bit_stage);
+        mark("uploads");
         DevInst& d = I->d;
         d.J = J;
         d.S = S;
@@ -472,6 +486,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("FFSGA_STEP_MIX")) I->step_mix = std::max(0, std::atoi(v));
+        mark("devinst");
         int rc = eval_config(d, I->sm_count, d.max_warps, true, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
@@ -490,6 +505,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
         rc = eval_config(d, I->sm_count, step_warps, false, &I->ec_step);
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
+        mark("eval_config");
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&I->fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I->join, cudaEventDisableTiming));
@@ -500,6 +516,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         I->wl_count.alloc(2 * sizeof(long long));  // one item counter per joint-step group (grown on demand)
         I->eval_total.alloc(sizeof(unsigned long long));
         CK(cudaMemsetAsync(I->eval_total.p, 0, sizeof(unsigned long long), I->stream));
+        mark("streams+events+bufs");
         *out = hold.release();
     });
 }
