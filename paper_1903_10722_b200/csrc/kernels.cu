@@ -1410,7 +1410,8 @@ int eval_config(const DevInst& I, int sm_count, int warps_cap, bool early, EvalC
     // shared memory (large J), wider groups put fewer chromosomes in a warp (idle lanes) so that
     // one chromosome may use up to a whole CTA's shared memory.
     int rc = -3;
-    if (I.maxM <= 4 && (rc = eval_config_g<4>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
+    const int gmin = getenv("FFSGA_EVAL_G") ? atoi(getenv("FFSGA_EVAL_G")) : 0;  // experiments
+    if (I.maxM <= 4 && gmin <= 4 && (rc = eval_config_g<4>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
     if (I.maxM <= 8 && (rc = eval_config_g<8>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
     if (I.maxM <= 16 && (rc = eval_config_g<16>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
     if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, warps_cap, early, cfg);

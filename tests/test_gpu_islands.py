@@ -43,6 +43,7 @@ def test_cellular_init_and_slots(capi, orc):
     (6, 2, 2, 2, 4, 4, 1, 0.05, 1.0),
     (8, 3, 2, 4, 2, 2, 1, 0.3, 0.5),         # folded torus neighbourhoods
     (30, 4, 2, 8, 8, 6, 2, 0.2, 0.9),        # radius 2
+    (16, 3, 2, 4, 9, 9, 4, 0.1, 0.8),        # radius 4: 40 neighbours (more than a warp's lanes)
     (50, 6, 2, 5, 5, 5, 1, 1.0, 1.0),        # every gene mutates
     (12, 3, 2, 3, 6, 2, 1, 0.0, 0.0),        # no crossover, no mutation
 ])
