@@ -490,20 +490,16 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         int rc = eval_config(d, I->sm_count, d.max_warps, true, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
-        // A shared-memory-bound CTA of 8-15 warps runs better as two half-size CTAs per SM (the
-        // groups of a CTA pace each other at every stage; halves drift apart and overlap their
-        // stage tails): 500x20 9.18 -> 9.36 M evals/s.
-        if (d.max_warps == 0 && I->ec.warps >= 8 && I->ec.warps < 16) {
-            rc = eval_config(d, I->sm_count, I->ec.warps / 2, true, &I->ec);
-            if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
-        }
         // The joint GA step runs the cellular and the pseudo decoder launches side by side on two
         // streams: half-size CTAs let them share every SM instead of queueing behind each other
         // (measured at C3: 136.8 vs 127.9 generations/s with one full-size CTA per SM).
         // (small CTAs of large instances -- J = 1000: 4 warps -- gain nothing: kept whole)
         int step_warps = I->ec.warps >= 8 ? I->ec.warps / 2 : I->ec.warps;
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
-        rc = eval_config(d, I->sm_count, step_warps, false, &I->ec_step);
+        // Pop order: successor loads before the retire (measured with the two-pop pipeline:
+        // C3 149.0 vs 139.0 generations/s for the other order).  FFSGA_STEP_LATE: experiments.
+        const bool step_early = std::getenv("FFSGA_STEP_LATE") == nullptr;
+        rc = eval_config(d, I->sm_count, step_warps, step_early, &I->ec_step);
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         mark("eval_config");
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));

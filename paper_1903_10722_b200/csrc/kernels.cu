@@ -156,66 +156,81 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     }
     stage_barrier(I.cta_sync);
     if (work && m < Ms) {
-        // Software pipelined by one pop: pop i is retired (recurrence, list append, stores) at
-        // the top of iteration i+1, so its processing-time and gene-row loads have a whole head
-        // insertion to arrive, and retiring before the next loads lets each pending value
-        // reuse its register (no copy that would wait on the load).  The deferred stores cannot
-        // alias iteration i+1's loads: they touch dispatched jobs or list dummies only.
+        // Software pipelined by two pops: pop i is retired (recurrence, list append, stores) in
+        // iteration i+2, so its processing-time load (an L1 miss whenever the stage slice does
+        // not fit L1, i.e. an L2 round trip) has two head insertions to arrive.  The loop is
+        // unrolled twice with one pending slot per half (A, B): each half retires the slot it
+        // is about to refill -- the oldest pending pop -- and then loads straight into it, so
+        // no register copy waits on a load (a copy at the loop end did: a third of all K1 stall
+        // samples once sat on one IMAD.MOV behind the procT load).  The successor link/value of
+        // the popped job is loaded before the retire (EARLY, standalone launches) or after it
+        // (the joint GA step, where two decoder launches share the SMs); either way the
+        // retire's stores cannot alias it: the popped job has not been dispatched at this stage,
+        // so it is neither a tail nor a dummy of the stage's outgoing lists.
         double avail = 0.0;
-        double q_br = 0.0, q_p = 0.0;  // pending pop: ready time and processing time
-        int q_j = END, q_g = 0;
-        auto retire = [&]() {
-            const double start = (q_br < avail) ? avail : q_br;  // std::max(ready, avail)
-            const double c = __dadd_rn(start, q_p);
+        struct Pend {
+            double br, p;  // ready time, processing time
+            int g, j;      // next-stage gene, job (END: empty)
+        };
+        Pend A{0.0, 0.0, 0, END}, B{0.0, 0.0, 0, END};
+        auto retire = [&](const Pend& q) {
+            const double start = (q.br < avail) ? avail : q.br;  // std::max(ready, avail)
+            const double c = __dadd_rn(start, q.p);
             avail = c;
             if (SCHED) {
-                const int at = q_j * I.S + s;
+                const int at = q.j * I.S + s;
                 W.smachine[at] = m;
                 W.sstart[at] = start;
                 W.scomp[at] = c;
             }
             if (!last) {
-                const int d = min(q_g, G - 1);
+                const int d = min(q.g, G - 1);
                 const int t = mytail[d];
-                link[t] = (uint16_t)q_j;
+                link[t] = (uint16_t)q.j;
                 lval[t] = c;
-                mytail[d] = (uint16_t)q_j;
+                mytail[d] = (uint16_t)q.j;
             } else {
-                lval[q_j] = c;  // final completion (the node was consumed by its pop)
+                lval[q.j] = c;  // final completion (the node was consumed by its pop)
             }
         };
-        while (true) {
-            const int bj = hj[0];
-            if (bj == END) break;
+        // one pop into slot q (which holds the oldest pending pop, retired first)
+        auto pop = [&](Pend& q, int bj) {
+            int nh;
+            double nr;
             if (EARLY) {
-                // This pop's loads go first, ahead of the previous pop's retire: bj has not been
-                // dispatched yet, so it is neither a tail nor a dummy of this stage's outgoing
-                // lists and the retire's stores cannot touch link[bj] / lval[bj]; written in this
-                // order the compiler issues the loads before the retire's store chain.  Faster
-                // for a launch that owns the GPU (+2-10 %), slower (-2.5 %) when two decoder
-                // launches share the SMs in the joint GA step, which uses the other order.
-                const int nh = link[bj];
-                const double nr = lval[bj];
-                const double p_now = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32
-                const int g_now = last ? 0 : (int)row[bj];
-                if (q_j != END) retire();
-                q_br = hv[0];
-                q_p = p_now;
-                q_g = g_now;
-                q_j = bj;
-                heads_replace_min<NS>(hv, hj, nr, nh);
-            } else {
-                if (q_j != END) retire();
-                q_br = hv[0];
-                q_p = __ldg(pcol + (unsigned)bj);
-                q_g = last ? 0 : (int)row[bj];
-                q_j = bj;
-                const int nh = link[bj];
-                const double nr = lval[bj];
-                heads_replace_min<NS>(hv, hj, nr, nh);
+                nh = link[bj];
+                nr = lval[bj];
             }
+            if (q.j != END) retire(q);
+            q.br = hv[0];
+            q.p = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32
+            q.g = last ? 0 : (int)row[bj];
+            q.j = bj;
+            if (!EARLY) {
+                nh = link[bj];
+                nr = lval[bj];
+            }
+            heads_replace_min<NS>(hv, hj, nr, nh);
+        };
+        bool a_older = true;  // which pending slot holds the older pop at loop exit
+        while (true) {
+            int bj = hj[0];
+            if (bj == END) break;
+            pop(A, bj);
+            bj = hj[0];
+            if (bj == END) {
+                a_older = false;
+                break;
+            }
+            pop(B, bj);
         }
-        if (q_j != END) retire();
+        if (a_older) {
+            if (A.j != END) retire(A);
+            if (B.j != END) retire(B);
+        } else {
+            if (B.j != END) retire(B);
+            if (A.j != END) retire(A);
+        }
         if (!last) {
 #pragma unroll
             for (int d = 0; d < G; ++d) {
@@ -1360,6 +1375,12 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, bool early, Eva
     const size_t per_warp = (size_t)(32 / G) * cfg->gl.bytes;
     int warps = (int)std::min<size_t>(warps_cap > 0 ? warps_cap : 16, max_smem / per_warp);
     if (warps < 1) return -1;
+    // Leave at least ~27 KB of the unified L1 to the stage's processing-time slice when that
+    // costs no more than one warp: the pop loop's procT loads then mostly hit L1 (500x20: one
+    // 8-warp CTA 9.86 M evals/s, 9 warps 9.34, two 4-warp CTAs 9.37 -- two CTAs pull two
+    // stage slices through the same L1).
+    const int pref = (int)((200 * 1024) / per_warp);
+    if (pref >= 1) warps = std::min(warps, pref);
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
     cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
