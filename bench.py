@@ -325,7 +325,7 @@ def main():
         try:
             with open(os.path.join(ROOT, "profiles", "r1_ncu.json")) as f:
                 for k in json.load(f)["kernels"]:
-                    if "k_eval<8, 0>" in k["kernel"]:
+                    if "k_eval<8, 0" in k["kernel"]:
                         ia = k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0
                         issue = {"bound": "issue", "frac": ia, "unit": "warp instructions/cycle/SMSP",
                                  "achieved": ia, "peak": 1.0,
