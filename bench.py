@@ -337,8 +337,11 @@ def main():
 
         # e2e: the public API call a user makes (instance upload, island init, K generations,
         # traces + champion back to the host), wall clock; median of E2E_RUNS independent runs
+        # one untimed end-to-end run first: the process's first model pays one-time costs (lazy
+        # kernel-module loading, growth of the stream-ordered memory pool to the model's 0.8 GB)
+        # that a serving process does not pay per request
         runs = []
-        for _ in range(E2E_RUNS):
+        for it in range(E2E_RUNS + 1):
             barrier()
             t0 = time.perf_counter()
             inst2, emax2 = make_instance()
@@ -349,9 +352,10 @@ def main():
             res = model2.run()
             barrier()
             t2 = time.perf_counter()
-            runs.append((t2 - t0, t1 - t0, t2 - t1, model2.inst.last_step_ms() / 1e3))
+            if it > 0:
+                runs.append((t2 - t0, t1 - t0, t2 - t1, model2.inst.last_step_ms() / 1e3))
             del model2
-            if os.environ.get("FFSGA_BENCH_DEBUG"):
+            if os.environ.get("FFSGA_BENCH_DEBUG") and runs:
                 print("e2e run", runs[-1], file=sys.stderr, flush=True)
         if comm is not None:  # max over ranks, per run
             agg = comm.allgather(np.array([r[0] for r in runs]))
@@ -395,7 +399,7 @@ def main():
                 "e2e": {"value": args.steps / e2e_s, "unit": "generations/s",
                         "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                         "what": "generate instance + IslandModel init + run(K generations) + traces/champion D2H; "
-                                "median of %d runs in one process" % E2E_RUNS,
+                                "median of %d runs in one process after one untimed run" % E2E_RUNS,
                         "parts": e2e_parts,
                         "best_objective": res.best_report["objective"]},
                 "gpu_launches": int(l1 - l0),
