@@ -156,7 +156,7 @@ struct ffsga_cuda_instance_t {
     DevInst d{};
     DevBuf dM, dStageOff, dBps, dSbo, dProcT, dRelease, dDue, dRelOrder, dBitStage;
     EvalConfig ec{};       // standalone batches: full-size CTAs
-    EvalConfig ec_step{};  // joint GA step: half-size CTAs (two decoder launches share the SMs)
+    EvalConfig ec_step{};  // joint GA step (FFSGA_STEP_WARPS / FFSGA_STEP_LATE: experiments)
     cudaStream_t stream = nullptr;
     std::vector<cudaStream_t> side;      // joint step: streams of step groups 1.. (group 0: stream)
     std::vector<cudaEvent_t> side_join;
@@ -491,10 +491,10 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         // The joint GA step runs the cellular and the pseudo decoder launches side by side on two
-        // streams: half-size CTAs let them share every SM instead of queueing behind each other
-        // (measured at C3: 136.8 vs 127.9 generations/s with one full-size CTA per SM).
-        // (small CTAs of large instances -- J = 1000: 4 warps -- gain nothing: kept whole)
-        int step_warps = I->ec.warps >= 8 ? I->ec.warps / 2 : I->ec.warps;
+        // streams.  With the two-pop pipeline the standalone CTA (one per SM, L1 left for the
+        // procT slice) is also the best step CTA: C3 152.5 generations/s vs 148.7 with half-size
+        // CTAs that let both launches share an SM (which won before the pipeline: 136.8 vs 127.9).
+        int step_warps = I->ec.warps;
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
         // Pop order: successor loads before the retire (measured with the two-pop pipeline:
         // C3 149.0 vs 139.0 generations/s for the other order).  FFSGA_STEP_LATE: experiments.
