@@ -491,10 +491,12 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         // The joint GA step runs the cellular and the pseudo decoder launches side by side on two
-        // streams.  With the two-pop pipeline the standalone CTA (one per SM, L1 left for the
-        // procT slice) is also the best step CTA: C3 152.5 generations/s vs 148.7 with half-size
-        // CTAs that let both launches share an SM (which won before the pipeline: 136.8 vs 127.9).
-        int step_warps = I->ec.warps;
+        // streams.  With the two-pop pipeline a shared-memory-bound standalone CTA (one per SM,
+        // L1 left for the procT slice) is also the best step CTA: C3 152.5 generations/s vs 148.7
+        // with half-size CTAs that let both launches share an SM (which won before the
+        // pipeline: 136.8 vs 127.9).  Small instances, whose standalone CTA is the 16-warp cap,
+        // still do better with half-size CTAs (C2: 11.3 k vs 8.7 k generations/s).
+        int step_warps = I->ec.warps > 8 ? I->ec.warps / 2 : I->ec.warps;
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
         // Pop order: successor loads before the retire (measured with the two-pop pipeline:
         // C3 149.0 vs 139.0 generations/s for the other order).  FFSGA_STEP_LATE: experiments.
