@@ -858,19 +858,58 @@ __device__ __forceinline__ unsigned extract_gene(const unsigned long long* wv, i
     return val >= M ? val - M : val;
 }
 
-// One job per lane: a job's slots are contiguous, and the 32 lanes of a warp write 32
-// consecutive bytes of each stage row.
+// Four consecutive jobs per lane: a job's slots are contiguous, so when its bits fit 128
+// (bits_per_job <= 128, e.g. 48 at 500x20x[2,8]) the lane loads the three words that can hold
+// them once and cuts every gene out of a 128-bit register window; the four genes of a stage go
+// out as one 32-bit store (the 32 lanes of a warp write 128 consecutive bytes of each stage row).
+// Wider jobs read the words per gene.
+__device__ __forceinline__ unsigned window_gene(unsigned long long lo, unsigned long long hi, int o, int nb,
+                                                unsigned M) {
+    const unsigned long long x = o >= 64 ? hi >> (o - 64) : (o ? (lo >> o) | (hi << (64 - o)) : lo);
+    const unsigned raw = (unsigned)(x & ((1ull << nb) - 1ull));  // bit o at position 0
+    const unsigned val = __brev(raw) >> (32 - nb);               // bit o becomes the MSB
+    return val >= M ? val - M : val;
+}
+
 __device__ __forceinline__ void unpack_member(const DevInst& I, const unsigned long long* wv, uint8_t* dst,
                                               int lane) {
-    for (int j = lane; j < I.Jpad; j += 32) {
-        if (j >= I.J) {
-            for (int s = 0; s < I.S; ++s) dst[(size_t)s * I.Jpad + j] = 0;
-            continue;
+    if (I.bits_per_job > 128) {
+        for (int j = lane; j < I.Jpad; j += 32) {
+            const int base = j * I.bits_per_job;
+            for (int s = 0; s < I.S; ++s)
+                dst[(size_t)s * I.Jpad + j] =
+                    j < I.J ? (uint8_t)extract_gene(wv, base + __ldg(I.sbo + s), __ldg(I.bps + s),
+                                                    (unsigned)__ldg(I.M + s))
+                            : (uint8_t)0;
         }
-        const int base = j * I.bits_per_job;
-        for (int s = 0; s < I.S; ++s)
-            dst[(size_t)s * I.Jpad + j] =
-                (uint8_t)extract_gene(wv, base + __ldg(I.sbo + s), __ldg(I.bps + s), (unsigned)__ldg(I.M + s));
+        return;
+    }
+    for (int q = lane; q < I.Jpad / 4; q += 32) {
+        unsigned long long lo[4], hi[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = 4 * q + u;
+            lo[u] = hi[u] = 0ull;
+            if (j < I.J) {
+                const int base = j * I.bits_per_job;
+                const int w0 = base >> 6, sh = base & 63;
+                const unsigned long long a = wv[w0];
+                const unsigned long long b = w0 + 1 < I.words ? wv[w0 + 1] : 0ull;
+                const unsigned long long c = w0 + 2 < I.words ? wv[w0 + 2] : 0ull;
+                lo[u] = sh ? (a >> sh) | (b << (64 - sh)) : a;  // bits [base, base + 64)
+                hi[u] = sh ? (b >> sh) | (c << (64 - sh)) : b;  // bits [base + 64, base + 128)
+            }
+        }
+        const int valid = min(4, I.J - 4 * q);  // jobs past J are zero bytes
+        for (int s = 0; s < I.S; ++s) {
+            const int o = __ldg(I.sbo + s), nb = __ldg(I.bps + s);
+            const unsigned M = (unsigned)__ldg(I.M + s);
+            unsigned v = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < valid) v |= window_gene(lo[u], hi[u], o, nb, M) << (8 * u);
+            reinterpret_cast<unsigned*>(dst + (size_t)s * I.Jpad)[q] = v;
+        }
     }
 }
 

@@ -94,7 +94,9 @@ def check_pseudo(dp, op):
 
 @pytest.mark.parametrize("J,S,lo,hi,n,xr", [
     (6, 2, 2, 2, 16, 0.75), (20, 5, 3, 3, 64, 0.75), (13, 7, 2, 8, 40, 1.0), (100, 10, 2, 5, 128, 0.75),
-    (9, 3, 1, 5, 2, 0.5), (30, 20, 2, 8, 32, 0.0)])
+    (9, 3, 1, 5, 2, 0.5), (30, 20, 2, 8, 32, 0.0),
+    (40, 25, 9, 16, 32, 0.75),   # 100 bits per job: the unpack window's upper word
+    (11, 30, 17, 32, 24, 0.9)])  # 150 bits per job: wider than the 128-bit unpack window
 def test_pseudo_steps_match_oracle(capi, orc, J, S, lo, hi, n, xr):
     d = synthetic(orc, J, S, lo, hi)
     oi = orc.instance(d)
