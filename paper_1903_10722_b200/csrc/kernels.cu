@@ -93,11 +93,14 @@ __device__ __forceinline__ void heads_sort(double (&v)[NS], int (&j)[NS]) {
     }
 }
 
-template <int NS>
+// EXACT: (ready, job) order.  Otherwise ready times only (one compare per head instead of
+// three); equal ready times then pop back to back in some order, which stage_pass detects, and
+// the chromosome is decoded again with the exact order (never for continuous processing times).
+template <int NS, bool EXACT>
 __device__ __forceinline__ void heads_replace_min(double (&v)[NS], int (&j)[NS], double x, int xj) {
     bool c[NS];
 #pragma unroll
-    for (int k = 0; k + 1 < NS; ++k) c[k] = key_lt(v[k + 1], j[k + 1], x, xj);
+    for (int k = 0; k + 1 < NS; ++k) c[k] = EXACT ? key_lt(v[k + 1], j[k + 1], x, xj) : (v[k + 1] < x);
     double nv[NS];
     int nj[NS];
 #pragma unroll
@@ -130,11 +133,11 @@ __device__ __forceinline__ void stage_barrier(bool cta) {
         __syncwarp();
 }
 
-template <int G, int NS, bool SCHED, bool LAST, bool EARLY>
+template <int G, int NS, bool SCHED, bool LAST, bool EARLY, bool EXACT>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                            int m, bool work, double* __restrict__ lval,
                                            uint16_t* __restrict__ link, uint16_t* __restrict__ tail,
-                                           const uint8_t* __restrict__ row, const EvalItems& W) {
+                                           const uint8_t* __restrict__ row, const EvalItems& W, bool& tie) {
     const int J = I.J;
     const int END = J;
     constexpr bool last = LAST;
@@ -172,7 +175,10 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             double br, p;  // ready time, processing time
             int g, j;      // next-stage gene, job (END: empty)
         };
-        Pend A{0.0, 0.0, 0, END}, B{0.0, 0.0, 0, END};
+        // ready times of the two pending pops; NaN (equal to nothing) until a slot is filled
+        const double qnan = __longlong_as_double(0x7FF8000000000000LL);
+        Pend A{qnan, 0.0, 0, END}, B{qnan, 0.0, 0, END};
+        bool eq = false;  // two consecutive pops with equal ready times (ready-only order)
         auto retire = [&](const Pend& q) {
             const double start = (q.br < avail) ? avail : q.br;  // std::max(ready, avail)
             const double c = __dadd_rn(start, q.p);
@@ -194,7 +200,8 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
         };
         // one pop into slot q (which holds the oldest pending pop, retired first)
-        auto pop = [&](Pend& q, int bj) {
+        auto pop = [&](Pend& q, const Pend& prev, int bj) {
+            if (!EXACT) eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
             int nh;
             double nr;
             if (EARLY) {
@@ -210,20 +217,21 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 nh = link[bj];
                 nr = lval[bj];
             }
-            heads_replace_min<NS>(hv, hj, nr, nh);
+            heads_replace_min<NS, EXACT>(hv, hj, nr, nh);
         };
         bool a_older = true;  // which pending slot holds the older pop at loop exit
         while (true) {
             int bj = hj[0];
             if (bj == END) break;
-            pop(A, bj);
+            pop(A, B, bj);
             bj = hj[0];
             if (bj == END) {
                 a_older = false;
                 break;
             }
-            pop(B, bj);
+            pop(B, A, bj);
         }
+        tie |= eq;
         if (a_older) {
             if (A.j != END) retire(A);
             if (B.j != END) retire(B);
@@ -243,17 +251,20 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     stage_barrier(I.cta_sync);
 }
 
-template <int G, bool SCHED, bool EARLY>
+template <int G, bool SCHED, bool EARLY, bool EXACT>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                                int m, bool work, double* lval, uint16_t* link,
-                                               uint16_t* tail, const uint8_t* row, const EvalItems& W) {
+                                               uint16_t* tail, const uint8_t* row, const EvalItems& W,
+                                               bool& tie) {
 #define FFSGA_STAGE(NS_)                                                                           \
     if constexpr (NS_ <= G) {                                                                       \
         if (Mprev <= NS_) {                                                                         \
             if (Mnext)                                                                              \
-                stage_pass<G, NS_, SCHED, false, EARLY>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W); \
+                stage_pass<G, NS_, SCHED, false, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                                                               row, W, tie);                        \
             else                                                                                    \
-                stage_pass<G, NS_, SCHED, true, EARLY>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W);  \
+                stage_pass<G, NS_, SCHED, true, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                                                              row, W, tie);                         \
             return;                                                                                 \
         }                                                                                           \
     }
@@ -336,91 +347,110 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
          base += (long long)gridDim.x * groups_per_cta) {
         const long long item = base + gid;
         const bool active = item < n;
-        const uint8_t* genes = nullptr;
-        if (active) {
-            genes = W.ptrs ? W.ptrs[item] : W.base + item * W.stride;
-            prefetch_row<G>(I, genes, 0, m, row_a);
-        }
-        tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
-        __pipeline_wait_prior(0);
-        __syncwarp();
+        const uint8_t* genes = active ? (W.ptrs ? W.ptrs[item] : W.base + item * W.stride) : nullptr;
 
-        // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order;
-        // node values are release times.  G consecutive jobs are linked per match_any.
-        const int M0 = I.M[0];
-        int bad_k = 0x7FFFFFFF;
-        for (int b0 = 0; b0 < J; b0 += G) {
-            const int k = b0 + m;
-            const bool valid = active && k < J;
-            const int j = valid ? (int)I.rel_order[k] : 0;
-            const int d = valid ? (int)row_a[j] : 0;
-            const bool good = valid && d < M0;
-            if (valid && !good) bad_k = min(bad_k, k);
-            const double rel = valid ? __ldg(I.release + j) : 0.0;
-            const unsigned key = good ? (((unsigned)gw << 8) | (unsigned)d) : (0x10000u | (unsigned)lane);
-            const unsigned peers = __match_any_sync(kFull, key);
-            const unsigned below = peers & ((1u << lane) - 1u);
-            const unsigned above = peers & ~((2u << lane) - 1u);
-            const int pred_lane = below ? (31 - __clz(below)) : lane;
-            const int pred_j = __shfl_sync(kFull, j, pred_lane);
-            int t = 0;
-            if (good && !below) t = tail[d];
+        // One decode of the group's chromosome (stage-0 routing, then every stage).  `work`
+        // enters as "decode this group" and leaves false when a gene is out of range; `tie`
+        // reports equal consecutive ready times under the ready-only pop order.
+        auto decode = [&](auto exact_tag, bool& work, bool& tie) {
+            constexpr bool EXACT = decltype(exact_tag)::value;
+            if (work) prefetch_row<G>(I, genes, 0, m, row_a);
+            tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
+            __pipeline_wait_prior(0);
             __syncwarp();
-            if (good) {
-                const int node = below ? pred_j : t;
-                link[node] = (uint16_t)j;
-                lval[node] = rel;
-            }
-            if (good && !above) tail[d] = (uint16_t)j;
-            __syncwarp();
-        }
-        if (active) {
-            const int t = tail[m];
-            link[t] = (uint16_t)END;
-            lval[t] = dinf();
-        }
-        bad_k = group_min_int<G>(bad_k);
-        bool work = active;
-        if (active && bad_k != 0x7FFFFFFF) {
-            work = false;
-            if (m == 0 && W.err)
-                atomicMin(W.err, ((unsigned long long)item << 32) | (unsigned long long)I.rel_order[bad_k]);
-        }
 
-        // ---- stages
-        int Mprev = 1;
-        for (int s = 0; s < S; ++s) {
-            const int Ms = I.M[s];
-            const int Mnext = (s + 1 < S) ? I.M[s + 1] : 0;
-            const uint8_t* row = row_a;
-            __syncwarp();  // every lane is done with row s
-            if (work && s + 1 < S) prefetch_row<G>(I, genes, s + 1, m, row_a);
-            if (work && s + 2 < S)  // warm L2 with row s+2 (no shared memory spent on it)
-                for (int v = m; v * 128 < I.Jpad; v += G)
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(genes + (size_t)(s + 2) * I.Jpad + v * 128));
-            __pipeline_wait_prior(0);  // row s+1 has landed
-            __syncwarp();
-            bool row_bad = false;
-            if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
-            dispatch_stage<G, SCHED, EARLY>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W);
-            if (__any_sync(kFull, row_bad)) {
-                // first offending job in stage s+1 dispatch order: min (ready, job) among them
-                BadTrack bad;
-                bad.reset();
-                if (row_bad && work) find_bad<G>(I, m, Ms, Mnext, lval, link, row, bad);
-                double bc = bad.c;
-                int bj = bad.j;
-                group_min_key<G>(bc, bj);
-                if (row_bad && work && bj != 0x7FFFFFFF) {
-                    work = false;
-                    if (m == 0 && W.err)
-                        atomicMin(W.err, ((unsigned long long)item << 32) |
-                                             ((unsigned long long)(s + 1) << 16) | (unsigned long long)bj);
+            // ---- stage-0 routing: release order (model.cpp:98-105) split per machine, in order;
+            // node values are release times.  G consecutive jobs are linked per match_any.
+            const int M0 = I.M[0];
+            int bad_k = 0x7FFFFFFF;
+            for (int b0 = 0; b0 < J; b0 += G) {
+                const int k = b0 + m;
+                const bool valid = work && k < J;
+                const int j = valid ? (int)I.rel_order[k] : 0;
+                const int d = valid ? (int)row_a[j] : 0;
+                const bool good = valid && d < M0;
+                if (valid && !good) bad_k = min(bad_k, k);
+                const double rel = valid ? __ldg(I.release + j) : 0.0;
+                const unsigned key = good ? (((unsigned)gw << 8) | (unsigned)d) : (0x10000u | (unsigned)lane);
+                const unsigned peers = __match_any_sync(kFull, key);
+                const unsigned below = peers & ((1u << lane) - 1u);
+                const unsigned above = peers & ~((2u << lane) - 1u);
+                const int pred_lane = below ? (31 - __clz(below)) : lane;
+                const int pred_j = __shfl_sync(kFull, j, pred_lane);
+                int t = 0;
+                if (good && !below) t = tail[d];
+                __syncwarp();
+                if (good) {
+                    const int node = below ? pred_j : t;
+                    link[node] = (uint16_t)j;
+                    lval[node] = rel;
                 }
+                if (good && !above) tail[d] = (uint16_t)j;
+                __syncwarp();
             }
-            Mprev = Ms;
+            if (work) {
+                const int t = tail[m];
+                link[t] = (uint16_t)END;
+                lval[t] = dinf();
+            }
+            bad_k = group_min_int<G>(bad_k);
+            if (work && bad_k != 0x7FFFFFFF) {
+                work = false;
+                if (m == 0 && W.err)
+                    atomicMin(W.err, ((unsigned long long)item << 32) | (unsigned long long)I.rel_order[bad_k]);
+            }
+
+            // ---- stages
+            int Mprev = 1;
+            for (int s = 0; s < S; ++s) {
+                const int Ms = I.M[s];
+                const int Mnext = (s + 1 < S) ? I.M[s + 1] : 0;
+                const uint8_t* row = row_a;
+                __syncwarp();  // every lane is done with row s
+                if (work && s + 1 < S) prefetch_row<G>(I, genes, s + 1, m, row_a);
+                if (work && s + 2 < S)  // warm L2 with row s+2 (no shared memory spent on it)
+                    for (int v = m; v * 128 < I.Jpad; v += G)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(genes + (size_t)(s + 2) * I.Jpad + v * 128));
+                __pipeline_wait_prior(0);  // row s+1 has landed
+                __syncwarp();
+                bool row_bad = false;
+                if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
+                dispatch_stage<G, SCHED, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W,
+                                                       tie);
+                if (__any_sync(kFull, row_bad)) {
+                    // first offending job in stage s+1 dispatch order: min (ready, job) among them
+                    BadTrack bad;
+                    bad.reset();
+                    if (row_bad && work) find_bad<G>(I, m, Ms, Mnext, lval, link, row, bad);
+                    double bc = bad.c;
+                    int bj = bad.j;
+                    group_min_key<G>(bc, bj);
+                    if (row_bad && work && bj != 0x7FFFFFFF) {
+                        work = false;
+                        if (m == 0 && W.err)
+                            atomicMin(W.err, ((unsigned long long)item << 32) |
+                                                 ((unsigned long long)(s + 1) << 16) | (unsigned long long)bj);
+                    }
+                }
+                Mprev = Ms;
+            }
+            __pipeline_wait_prior(0);
+        };
+
+        bool work = active, tie = false;
+        decode(std::false_type{}, work, tie);
+        // Equal ready times met under the ready-only order (integer-valued instances; never seen
+        // with continuous processing times): decode those chromosomes again in (ready, job)
+        // order.  CTA-uniform decision, because the stage passes contain CTA barriers.
+        const bool any_tie = I.cta_sync ? (__syncthreads_or(tie) != 0) : __any_sync(kFull, tie);
+        if (any_tie) {
+            unsigned gt = tie ? 1u : 0u;
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1) gt |= __shfl_xor_sync(kFull, gt, off, G);
+            bool redo = gt != 0 && work, tie2 = false;
+            decode(std::true_type{}, redo, tie2);
+            if (gt) work = redo;
         }
-        __pipeline_wait_prior(0);
 
         // ---- report_from_completions (model.cpp:107-120); completions are in lval[0..J)
         double mk = 0.0;
