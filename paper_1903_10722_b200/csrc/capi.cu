@@ -169,7 +169,7 @@ struct ffsga_cuda_instance_t {
     std::vector<const void*> graph_key;
     std::mutex mu;
     // joint-step work list
-    DevBuf wl_ptrs, wl_obj, wl_fit, wl_count, wl_scratch, cell_desc, pseudo_desc;
+    DevBuf wl_ptrs, wl_obj, wl_fit, wl_count, cell_desc, pseudo_desc;
     // evaluate() staging
     DevBuf ev_in, ev_rows, ev_obj, ev_fit, ev_mk, ev_td, ev_err;
     long long ev_cap = 0;
@@ -839,11 +839,11 @@ struct ffsga_cuda_pseudo_t {
     ffsga_cuda_instance_t* inst = nullptr;
     int n = 0;
     unsigned long long gen = 0;
-    DevBuf words, fit, obj, mslot, archive, st, trace, desc;
+    DevBuf words, fit, obj, mslot, rows, archive, st, trace, desc;
     long long trace_cap = 0;
     PseudoIsland d{};
     void adopt(cudaStream_t s) {
-        for (DevBuf* b : {&words, &fit, &obj, &mslot, &archive, &st, &trace, &desc}) b->owner = s;
+        for (DevBuf* b : {&words, &fit, &obj, &mslot, &rows, &archive, &st, &trace, &desc}) b->owner = s;
     }
     void push_desc() {
         d.trace = trace.as<double>();
@@ -1143,6 +1143,15 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         std::lock_guard<std::mutex> lk(inst->mu);
         ffsga_cuda_instance_t* I = inst;
         I->use();
+        const bool dbg = std::getenv("FFSGA_DEBUG_INIT") != nullptr;
+        auto t_last = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!dbg) return;
+            const auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "pseudo_create %-24s %.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(t - t_last).count());
+            t_last = t;
+        };
         auto* p = new ffsga_cuda_pseudo_t();
         std::unique_ptr<ffsga_cuda_pseudo_t> hold(p);
         p->inst = I;
@@ -1162,23 +1171,32 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         CK(cudaMemcpyAsync(p->st.p, &s0, sizeof(s0), cudaMemcpyHostToDevice, I->stream));  // pageable: staged
         p->trace_cap = 1;
         p->trace.alloc(sizeof(double));
-        // pairs (x, ~x): x = pair p's chromosome of the sequential init stream (pseudo.cpp:40-47)
+        mark("allocs");
+        // pairs (x, ~x): x = pair p's chromosome of the sequential init stream (pseudo.cpp:40-47).
+        // The island's row storage (gene rows of its crossed members in every generation) holds
+        // the initial members' rows for their first evaluation.  An island-sized buffer is
+        // recycled by the stream-ordered pool across models (a shared arena regrown by the first
+        // step was not: 10-45 ms to map per model).
         const size_t block = I->block();
-        I->wl_scratch.ensure(block * (size_t)population);  // shared scratch arena: no per-island malloc/free
-        uint8_t* rows = I->wl_scratch.as<uint8_t>();
+        p->rows.alloc(block * (size_t)population);
+        uint8_t* rows = p->rows.as<uint8_t>();
+        mark("rows");
         CK(launch_random_rows(I->d, rows, (long long)block, population / 2, seed, 0, false, I->stream));
         CK(launch_pack_bits(I->d, rows, (long long)block, nullptr, p->words.as<unsigned long long>(), nullptr,
                             population / 2, true, I->dBitStage.as<uint16_t>(), I->stream));
         CK(launch_unpack_rows(I->d, p->words.as<unsigned long long>(), nullptr, rows, (long long)block, nullptr,
                               population, I->stream));
         g_launches += 3;
+        mark("init launches");
         eval_rows(I, rows, population, p->obj.as<double>(), p->fit.as<double>(), nullptr, nullptr, false);
+        mark("eval_rows");
         PseudoIsland& d = p->d;  // (device-generated genes: in range by construction)
         d.n = population;
         d.words = p->words.as<unsigned long long>();
         d.fit = p->fit.as<double>();
         d.obj = p->obj.as<double>();
         d.mslot = p->mslot.as<long long>();
+        d.rows = p->rows.as<uint8_t>();
         d.archive = p->archive.as<unsigned long long>();
         d.seed = seed;
         d.thr_xr = coin_threshold(xr);
@@ -1186,6 +1204,7 @@ int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr
         d.pair0 = 0;
         p->push_desc();
         refresh_stats(nullptr, p, 2);  // archive = first max over the scored members
+        mark("stats");
         *out = hold.release();          // stream-ordered, as cellular_create
     });
 }
@@ -1371,16 +1390,15 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         struct Group {
             int c0, c1, p0, p1;
             long long cells, pairs;  // units of the group
-            long long item0, srow0;  // first work-list item, first pseudo scratch row
+            long long item0;  // first work-list item
         };
         std::vector<Group> groups;
         auto add_group = [&](int c0, int c1, int p0, int p1) {
-            Group G{c0, c1, p0, p1, cell_base[c1] - cell_base[c0], pair_base[p1] - pair_base[p0], 0, 0};
+            Group G{c0, c1, p0, p1, cell_base[c1] - cell_base[c0], pair_base[p1] - pair_base[p0], 0};
             if (G.cells + G.pairs == 0) return;
             if (!groups.empty()) {
                 const Group& L = groups.back();
                 G.item0 = L.item0 + L.cells + 2 * L.pairs;
-                G.srow0 = L.srow0 + 2 * L.pairs;
             }
             for (int i = c0; i < c1; ++i) cd[i].item0 = cd[i].cell0 = cell_base[i] - cell_base[c0];
             for (int i = p0; i < p1; ++i) pd[i].pair0 = pair_base[i] - pair_base[p0];
@@ -1401,7 +1419,6 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         I->wl_ptrs.ensure(sizeof(void*) * cap);
         I->wl_obj.ensure(sizeof(double) * cap);
         I->wl_fit.ensure(sizeof(double) * cap);
-        I->wl_scratch.ensure(std::max<size_t>(1, (size_t)(2 * n_pairs) * I->block()));
         I->wl_count.ensure(sizeof(long long) * std::max<size_t>(2, groups.size()));
         I->cell_desc.ensure(sizeof(CellIsland) * std::max(1, nc));
         I->pseudo_desc.ensure(sizeof(PseudoIsland) * std::max(1, np));
@@ -1437,8 +1454,6 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             w.fit = wfit + G.item0;
             w.count = I->wl_count.as<long long>() + k;  // gen-begin sets it to the group's cells
             w.total = I->eval_total.as<unsigned long long>();
-            w.scratch = I->wl_scratch.as<uint8_t>() + (size_t)G.srow0 * I->block();
-            w.scratch0 = G.cells;  // pseudo slot s -> scratch row s - cells
             EvalItems E{};
             E.ptrs = w.ptrs;
             E.obj = w.obj;
@@ -1493,7 +1508,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             // generations once (device-side generation counters make it replayable)
             const int chunk = std::min(generations, 16);
             const std::vector<const void*> key = {cdev, pdev, (const void*)ptrs, (const void*)wobj,
-                                                  I->wl_scratch.p, I->wl_count.p, (const void*)groups.size(),
+                                                  I->wl_count.p, (const void*)groups.size(),
                                                   (const void*)(intptr_t)nc, (const void*)(intptr_t)np,
                                                   (const void*)(intptr_t)n_cells, (const void*)(intptr_t)n_pairs,
                                                   (const void*)(intptr_t)chunk};

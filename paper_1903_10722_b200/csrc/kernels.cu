@@ -1187,7 +1187,7 @@ __global__ void k_cell_candidate(DevInst I, CellIsland C, int cell, unsigned lon
 // ---------------------------------------------------------------------------- K4 pseudo breed
 // pair_step (pseudo.cpp:11-29) for one pair per warp: coin, then one mask word per 64 bits,
 // children written in place; crossed members are appended to the evaluation work list with
-// their gene rows (bits_to_int, chromosome.cpp:44-59) in the scratch arena.
+// their gene rows (bits_to_int, chromosome.cpp:44-59) in the island's row storage.
 __global__ void __launch_bounds__(256) k_pseudo_breed(DevInst I, const PseudoIsland* __restrict__ isl,
                                                        int n_islands, long long n_pairs, WorkList wl) {
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1221,7 +1221,7 @@ __global__ void __launch_bounds__(256) k_pseudo_breed(DevInst I, const PseudoIsl
     slot = __shfl_sync(kFull, slot, 0);
     __syncwarp();
     const size_t block = (size_t)I.S * I.Jpad;
-    uint8_t* r1 = wl.scratch + (size_t)(slot - wl.scratch0) * block;
+    uint8_t* r1 = P.rows + (size_t)(2 * pair) * block;  // the island's own row storage
     uint8_t* r2 = r1 + block;
     unpack_member(I, A, r1, lane);
     unpack_member(I, B, r2, lane);

@@ -56,6 +56,7 @@ struct PseudoIsland {
     double* fit;                   // [n]
     double* obj;                   // [n]
     long long* mslot;              // [n] work item of a crossed member this generation, or -1
+    uint8_t* rows;                 // [n][S*Jpad] gene rows of the members crossed this generation
     unsigned long long* archive;   // [W]
     unsigned long long seed;
     unsigned long long thr_xr;
@@ -69,8 +70,6 @@ struct WorkList {
     double* obj;                   // [cap]
     double* fit;                   // [cap]
     long long* count;              // device counter
-    uint8_t* scratch;              // pseudo children rows [cap_pseudo][S*Jpad]
-    long long scratch0;            // item index of scratch row 0
     unsigned long long* total;     // running count of evaluations (optional)
 };
 
