@@ -38,6 +38,9 @@ def run(name, J, S, machines, couples, pop, mode, grid, steps):
           f"untimed wall {steps / wall:.1f} gen/s")
 
 
+if os.environ.get("ONLY_C4"):
+    run("C4 1000x20x[2,8], 32 couples x 1024", 1000, 20, bench.synthetic_machines(1000, 20), 32, 1024, "dual", (32, 32), 10)
+    sys.exit(0)
 run("C1 20x5x3, 1 cellular 16x16", 20, 5, [3] * 5, 1, 256, "cellular", (16, 16), 2000)
 run("C2 100x10x[2,5], dual 2048+2048", 100, 10, bench.synthetic_machines(100, 10, 2, 5), 1, 2048, "dual", (64, 32), 500)
 if os.environ.get("ONLY_SMALL"):
