@@ -262,6 +262,7 @@ void eval_rows(ffsga_cuda_instance_t* I, const uint8_t* rows, long long n, doubl
     W.n = n;
     W.base = rows;
     W.stride = (long long)I->block();
+    W.deal = 1;
     W.obj = obj;
     W.fit = fit;
     W.mk = mk;
@@ -737,6 +738,7 @@ int ffsga_cuda_batch_evaluate(ffsga_cuda_batch b, int64_t n) {
         W.n = n;
         W.base = b->rows.as<uint8_t>();
         W.stride = (long long)I->block();
+        W.deal = 1;
         W.obj = b->obj.as<double>();
         W.fit = b->fit.as<double>();
         W.mk = b->mk.as<double>();
@@ -1459,6 +1461,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             E.obj = w.obj;
             E.fit = w.fit;
             E.n_dev = w.count;
+            E.deal = groups.size() == 1 ? 1 : 0;  // a lone decoder launch owns the GPU
             ch.w = w;
             ch.E = E;
         }

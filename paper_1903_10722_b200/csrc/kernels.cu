@@ -342,10 +342,15 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
     const int END = J;
     const long long n = W.n_dev ? *W.n_dev + W.n : W.n;  // fused GA list: n cells + device count
 
-    // all groups of the CTA share the item loop (CTA-uniform bounds: stage barriers)
-    for (long long base = (long long)blockIdx.x * groups_per_cta; base < n;
-         base += (long long)gridDim.x * groups_per_cta) {
-        const long long item = base + gid;
+    // All groups of the CTA share the item loop (CTA-uniform bounds: stage barriers).  A launch
+    // that owns the GPU deals items round-robin over the CTAs (group g of CTA b takes item
+    // base + g * grid + b), so a final partial round spreads over every SM: a round lasts one
+    // chromosome's decode however many groups it holds, and thinly filled SMs decode faster.
+    // Launches sharing the GPU (joint GA step) take contiguous blocks instead, so CTAs without
+    // items in the last round exit and hand their SM to the other launch.
+    const long long stride = (long long)gridDim.x * groups_per_cta;
+    for (long long base = W.deal ? 0 : (long long)blockIdx.x * groups_per_cta; base < n; base += stride) {
+        const long long item = W.deal ? base + (long long)gid * gridDim.x + blockIdx.x : base + gid;
         const bool active = item < n;
         const uint8_t* genes = active ? (W.ptrs ? W.ptrs[item] : W.base + item * W.stride) : nullptr;
 

@@ -23,6 +23,7 @@ struct EvalItems {
     int* smachine;                 // K7 schedule of item 0 (job-major [j*S+s])
     double* sstart;
     double* scomp;
+    int deal;                      // 1: items round-robin over CTAs (launch owns the GPU)
 };
 
 struct IslandState {
