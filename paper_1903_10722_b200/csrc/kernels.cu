@@ -976,20 +976,10 @@ __device__ __forceinline__ unsigned long long shfl_max_u64(unsigned long long v)
     return v;
 }
 
-// Per-warp queue of one parse window's index draws (at most every other draw of a window).
-constexpr int kBreedWarps = 8;  // warps per CTA of the cellular breed launch
-struct MutQueue {
-    int n;
-    int gene[16 * kMutChunk + 1];
-    uint16_t off[16 * kMutChunk + 1];
-};
-
 // One cell, one warp: writes the child rows and returns the number of stream draws consumed.
 __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, int cell, unsigned long long cs,
                                          const double* __restrict__ fit, const uint8_t* __restrict__ selq,
-                                         uint8_t* __restrict__ child, int lane, MutQueue& q) {
-    if (lane == 0) q.n = 0;
-    __syncwarp();
+                                         uint8_t* __restrict__ child, int lane) {
     const int n = C.n;
     const int L = I.J * I.S;
     unsigned long long k = 0;
@@ -1144,35 +1134,17 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
         // index draws: right after a true coin (and draw 0 when the slice starts inside a pair)
         unsigned im = ((cm & tb) << 1) & ((1u << kMutChunk) - 1u);
         if (!st) im |= 1u;
-        // The index draws of the window are queued per warp (cheap per-lane enqueue), then drawn
-        // and applied 32 at a time by all lanes: the per-lane loop over one lane's draws would
-        // run the whole draw for the lane with the most of them while the others idle.
-        {
-            const int cnt = __popc(im);
-            int at = 0;
-            if (cnt) at = atomicAdd(&q.n, cnt);
-            while (im) {
-                const int t = __ffs(im) - 1;
-                im &= im - 1u;
-                q.gene[at] = g + __popc(cm & ((1u << t) - 1u)) - 1;
-                q.off[at] = (uint16_t)(lane * kMutChunk + t);
-                ++at;
+        while (im) {  // rare (mutation rate), divergent but short
+            const int t = __ffs(im) - 1;
+            im &= im - 1u;
+            const int gene = g + __popc(cm & ((1u << t) - 1u)) - 1;
+            if (gene < L) {
+                int j = (int)((double)gene * invS);  // gene / S without an integer divide
+                j -= (j * I.S > gene) ? 1 : 0;
+                j += ((j + 1) * I.S <= gene) ? 1 : 0;
+                const int s = gene - j * I.S;
+                child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(draw(cs, p0 + t), __ldg(I.M + s));
             }
-            __syncwarp();
-            const int total = q.n;
-            for (int e = lane; e < total; e += 32) {
-                const int gene = q.gene[e];
-                if (gene < L) {
-                    int j = (int)((double)gene * invS);  // gene / S without an integer divide
-                    j -= (j * I.S > gene) ? 1 : 0;
-                    j += ((j + 1) * I.S <= gene) ? 1 : 0;
-                    const int s = gene - j * I.S;
-                    child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(draw(cs, pos + q.off[e]), __ldg(I.M + s));
-                }
-            }
-            __syncwarp();
-            if (lane == 0) q.n = 0;
-            __syncwarp();
         }
         const int lF0 = __shfl_sync(kFull, F0, 31), lF1 = __shfl_sync(kFull, F1, 31);
         const int lC0 = __shfl_sync(kFull, C0, 31), lC1 = __shfl_sync(kFull, C1, 31);
@@ -1188,7 +1160,7 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
 // (one coin per gene plus one index draw per mutated gene, 148-150) is parsed warp-parallel:
 // draw k of the cell stream is mix(seed + (k+1) gamma), so each lane evaluates its slice of
 // the stream and a warp scan of the 2-state {coin, index} automaton assigns gene indices.
-__global__ void __launch_bounds__(32 * kBreedWarps) k_cell_breed(DevInst I, const CellIsland* __restrict__ isl,
+__global__ void __launch_bounds__(256) k_cell_breed(DevInst I, const CellIsland* __restrict__ isl,
                                                      int n_islands, long long n_cells, WorkList wl) {
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -1204,8 +1176,7 @@ __global__ void __launch_bounds__(32 * kBreedWarps) k_cell_breed(DevInst I, cons
     const unsigned long long gen_seed = derive_seed(C.seed, gen + 1ull);  // cellular.cpp:167
     const unsigned long long cs = derive_seed(gen_seed, (unsigned long long)cell);  // :171
     uint8_t* child = C.genes + ((size_t)(1 - selq[cell]) * n + cell) * ((size_t)I.S * I.Jpad);
-    __shared__ MutQueue mq[kBreedWarps];
-    breed_cell(I, C, cell, cs, C.fit + (size_t)q * n, selq, child, lane, mq[threadIdx.x >> 5]);
+    breed_cell(I, C, cell, cs, C.fit + (size_t)q * n, selq, child, lane);
     if (lane == 0) wl.ptrs[C.item0 + cell] = child;
 }
 
@@ -1213,9 +1184,8 @@ __global__ void __launch_bounds__(32 * kBreedWarps) k_cell_breed(DevInst I, cons
 __global__ void k_cell_candidate(DevInst I, CellIsland C, int cell, unsigned long long cs, int q, uint8_t* out,
                                  unsigned long long* draws) {
     const int lane = threadIdx.x & 31;
-    __shared__ MutQueue mq;
     const unsigned long long used =
-        breed_cell(I, C, cell, cs, C.fit + (size_t)q * C.n, C.sel + (size_t)q * C.n, out, lane, mq);
+        breed_cell(I, C, cell, cs, C.fit + (size_t)q * C.n, C.sel + (size_t)q * C.n, out, lane);
     if (lane == 0) *draws = used;
 }
 
@@ -1596,7 +1566,7 @@ cudaError_t launch_breed(const DevInst& I, const CellIsland* cells_dev, int nc, 
                          const PseudoIsland* pseudo_dev, int np, long long n_pairs, const WorkList& wl,
                          cudaStream_t st) {
     k_gen_begin<<<1, 1, 0, st>>>(wl.count, nc > 0 ? n_cells : 0);
-    if (n_cells > 0) k_cell_breed<<<blocks_for(n_cells * 32, 32 * kBreedWarps), 32 * kBreedWarps, 0, st>>>(I, cells_dev, nc, n_cells, wl);
+    if (n_cells > 0) k_cell_breed<<<blocks_for(n_cells * 32, 256), 256, 0, st>>>(I, cells_dev, nc, n_cells, wl);
     if (n_pairs > 0) k_pseudo_breed<<<blocks_for(n_pairs * 32, 256), 256, 0, st>>>(I, pseudo_dev, np, n_pairs, wl);
     return cudaGetLastError();
 }
