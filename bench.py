@@ -212,6 +212,16 @@ def ga_config(world):
             "l2": "inputs larger than L2 (resident population 0.77 GB > 126 MB)"}
 
 
+def sweep_traffic(n):
+    """DRAM bytes per sweep launch of n chromosomes, from the committed ncu capture (per-evaluation
+    figure of profiles/r1_sweep_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_sweep_traffic.json")) as f:
+            return json.load(f)["traffic_bytes_per_eval"] * n
+    except Exception:
+        return None
+
+
 def decoder_sweep(inst_data, emax, device, steps, warmup):
     """C5: 1M random chromosomes per launch (K2 fill, then K1 launches timed with events)."""
     from paper_1903_10722_b200 import capi
@@ -232,7 +242,7 @@ def decoder_sweep(inst_data, emax, device, steps, warmup):
     return {"evals_per_s": SWEEP_N / (avg / 1e3), "n_per_launch": SWEEP_N, "ms_per_launch": avg,
             "dispatches_per_s": SWEEP_N * L / (avg / 1e3),
             "roofline": {"bound": "hbm", "achieved": bytes_per / (avg / 1e3) / 1e9, "unit": "GB/s",
-                         "traffic": None, "algorithmic_bytes_per_launch": bytes_per},
+                         "traffic": sweep_traffic(SWEEP_N), "algorithmic_bytes_per_launch": bytes_per},
             "checksum_objective_sum": float(np.sum(obj))}
 
 
