@@ -156,7 +156,7 @@ struct ffsga_cuda_instance_t {
     DevInst d{};
     DevBuf dM, dStageOff, dBps, dSbo, dProcT, dRelease, dDue, dRelOrder, dBitStage;
     EvalConfig ec{};       // standalone batches: full-size CTAs
-    EvalConfig ec_step{};  // joint GA step (FFSGA_STEP_WARPS / FFSGA_STEP_LATE: experiments)
+    EvalConfig ec_step{};  // joint GA step (FFSGA_STEP_WARPS: experiments)
     cudaStream_t stream = nullptr;
     std::vector<cudaStream_t> side;      // joint step: streams of step groups 1.. (group 0: stream)
     std::vector<cudaEvent_t> side_join;
@@ -488,7 +488,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("FFSGA_STEP_MIX")) I->step_mix = std::max(0, std::atoi(v));
         mark("devinst");
-        int rc = eval_config(d, I->sm_count, d.max_warps, true, &I->ec);
+        int rc = eval_config(d, I->sm_count, d.max_warps, &I->ec);
         if (rc == -1) fail(FFSGA_ERR_CONFIG, "instance too large for the on-chip decoder state (num_jobs)");
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         // The joint GA step runs the cellular and the pseudo decoder launches side by side on two
@@ -499,10 +499,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         // still do better with half-size CTAs (C2: 11.3 k vs 8.7 k generations/s).
         int step_warps = I->ec.warps > 8 ? I->ec.warps / 2 : I->ec.warps;
         if (const char* v = std::getenv("FFSGA_STEP_WARPS")) step_warps = std::max(1, std::atoi(v));
-        // Pop order: successor loads before the retire (measured with the two-pop pipeline:
-        // C3 149.0 vs 139.0 generations/s for the other order).  FFSGA_STEP_LATE: experiments.
-        const bool step_early = std::getenv("FFSGA_STEP_LATE") == nullptr;
-        rc = eval_config(d, I->sm_count, step_warps, step_early, &I->ec_step);
+        rc = eval_config(d, I->sm_count, step_warps, &I->ec_step);
         if (rc != 0) fail(FFSGA_ERR_CUDA, std::string("decoder configuration failed: ") + cudaGetErrorString(cudaGetLastError()));
         mark("eval_config");
         CK(cudaStreamCreateWithFlags(&I->stream, cudaStreamNonBlocking));

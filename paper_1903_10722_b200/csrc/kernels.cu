@@ -133,7 +133,7 @@ __device__ __forceinline__ void stage_barrier(bool cta) {
         __syncwarp();
 }
 
-template <int G, int NS, bool SCHED, bool LAST, bool EARLY, bool EXACT>
+template <int G, int NS, bool SCHED, bool LAST, bool EARLY, bool EXACT, int DEPTH>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                            int m, bool work, double* __restrict__ lval,
                                            uint16_t* __restrict__ link, uint16_t* __restrict__ tail,
@@ -165,9 +165,9 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         // unrolled twice with one pending slot per half (A, B): each half retires the slot it
         // is about to refill -- the oldest pending pop -- and then loads straight into it, so
         // no register copy waits on a load (a copy at the loop end did: a third of all K1 stall
-        // samples once sat on one IMAD.MOV behind the procT load).  The successor link/value of
-        // the popped job is loaded before the retire (EARLY, standalone launches) or after it
-        // (the joint GA step, where two decoder launches share the SMs); either way the
+        // samples once sat on one IMAD.MOV behind the procT load).  DEPTH 3: three slots, three
+        // pops in flight.  The successor link/value of the popped job is loaded before the
+        // retire (EARLY; the other order measured 139.0 vs 149.0 C3 generations/s); the
         // retire's stores cannot alias it: the popped job has not been dispatched at this stage,
         // so it is neither a tail nor a dummy of the stage's outgoing lists.
         double avail = 0.0;
@@ -219,25 +219,61 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
             heads_replace_min<NS, EXACT>(hv, hj, nr, nh);
         };
-        bool a_older = true;  // which pending slot holds the older pop at loop exit
-        while (true) {
-            int bj = hj[0];
-            if (bj == END) break;
-            pop(A, B, bj);
-            bj = hj[0];
-            if (bj == END) {
-                a_older = false;
-                break;
+        if constexpr (DEPTH == 2) {
+            bool a_older = true;  // which pending slot holds the older pop at loop exit
+            while (true) {
+                int bj = hj[0];
+                if (bj == END) break;
+                pop(A, B, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    a_older = false;
+                    break;
+                }
+                pop(B, A, bj);
             }
-            pop(B, A, bj);
-        }
-        tie |= eq;
-        if (a_older) {
-            if (A.j != END) retire(A);
-            if (B.j != END) retire(B);
-        } else {
-            if (B.j != END) retire(B);
-            if (A.j != END) retire(A);
+            tie |= eq;
+            if (a_older) {
+                if (A.j != END) retire(A);
+                if (B.j != END) retire(B);
+            } else {
+                if (B.j != END) retire(B);
+                if (A.j != END) retire(A);
+            }
+        } else {  // three pops in flight (large J: the procT slice misses L1 more often)
+            Pend C{qnan, 0.0, 0, END};
+            int exit_at = 0;  // the slot the loop stopped before holds the oldest pending pop
+            while (true) {
+                int bj = hj[0];
+                if (bj == END) break;
+                pop(A, C, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    exit_at = 1;
+                    break;
+                }
+                pop(B, A, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    exit_at = 2;
+                    break;
+                }
+                pop(C, B, bj);
+            }
+            tie |= eq;
+            if (exit_at == 0) {
+                if (A.j != END) retire(A);
+                if (B.j != END) retire(B);
+                if (C.j != END) retire(C);
+            } else if (exit_at == 1) {
+                if (B.j != END) retire(B);
+                if (C.j != END) retire(C);
+                if (A.j != END) retire(A);
+            } else {
+                if (C.j != END) retire(C);
+                if (A.j != END) retire(A);
+                if (B.j != END) retire(B);
+            }
         }
         if (!last) {
 #pragma unroll
@@ -251,7 +287,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     stage_barrier(I.cta_sync);
 }
 
-template <int G, bool SCHED, bool EARLY, bool EXACT>
+template <int G, bool SCHED, bool EARLY, bool EXACT, int DEPTH>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                                int m, bool work, double* lval, uint16_t* link,
                                                uint16_t* tail, const uint8_t* row, const EvalItems& W,
@@ -260,10 +296,10 @@ __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mpre
     if constexpr (NS_ <= G) {                                                                       \
         if (Mprev <= NS_) {                                                                         \
             if (Mnext)                                                                              \
-                stage_pass<G, NS_, SCHED, false, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                stage_pass<G, NS_, SCHED, false, EARLY, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
                                                                row, W, tie);                        \
             else                                                                                    \
-                stage_pass<G, NS_, SCHED, true, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                stage_pass<G, NS_, SCHED, true, EARLY, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
                                                               row, W, tie);                         \
             return;                                                                                 \
         }                                                                                           \
@@ -326,7 +362,7 @@ __device__ __forceinline__ bool row_has_bad(const DevInst& I, const uint8_t* row
     return bad != 0;
 }
 
-template <int G, bool SCHED, bool EARLY>
+template <int G, bool SCHED, int DEPTH>
 __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
@@ -420,7 +456,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
                 __syncwarp();
                 bool row_bad = false;
                 if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
-                dispatch_stage<G, SCHED, EARLY, EXACT>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W,
+                dispatch_stage<G, SCHED, true, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W,
                                                        tie);
                 if (__any_sync(kFull, row_bad)) {
                     // first offending job in stage s+1 dispatch order: min (ready, job) among them
@@ -1439,7 +1475,7 @@ inline unsigned blocks_for(long long threads, int per_block) {
 }
 
 template <int G>
-int eval_config_g(const DevInst& I, int sm_count, int warps_cap, bool early, EvalConfig* cfg) {
+int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg) {
     (void)sm_count;
     cfg->G = G;
     cfg->gl = group_layout(I.J, I.Jpad, G);
@@ -1458,10 +1494,17 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, bool early, Eva
     cfg->warps = warps;
     cfg->groups_per_cta = 32 * warps / G;
     cfg->smem = (size_t)cfg->groups_per_cta * cfg->gl.bytes;
-    cfg->early = early;
-    const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false>
-                                 : (early ? (const void*)k_eval<G, false, true> : (const void*)k_eval<G, false, false>);
-    const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true, false>;
+    // Pop pipeline depth: three pops in flight for large instances (1000x20: +5 %), two
+    // otherwise (500x20: the third slot costs 1.5 %; 100x10: -32 %, registers bind there)
+    cfg->depth = 2;
+    const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false, 2>;
+    if constexpr (G == 8) {
+        if (I.algo != 1 && I.J >= 1000) {
+            cfg->depth = 3;
+            k0 = (const void*)k_eval<8, false, 3>;
+        }
+    }
+    const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true, 2>;
     // the opt-in ceiling, not this config's size: configs of other instances (other J) and the
     // joint-step config share the kernel's attribute
     cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -1489,27 +1532,31 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
         else
             k_eval_bkt<G, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.bl);
     } else if (schedule) {
-        k_eval<G, true, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
-    } else if (cfg.early) {
-        k_eval<G, false, true><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+        k_eval<G, true, 2><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
     } else {
-        k_eval<G, false, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+        if constexpr (G == 8) {
+            if (cfg.depth == 3) {
+                k_eval<8, false, 3><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                return cudaGetLastError();
+            }
+        }
+        k_eval<G, false, 2><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
     }
     return cudaGetLastError();
 }
 
 }  // namespace
 
-int eval_config(const DevInst& I, int sm_count, int warps_cap, bool early, EvalConfig* cfg) {
+int eval_config(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg) {
     // The smallest group that covers the widest stage; when a warp of such groups does not fit
     // shared memory (large J), wider groups put fewer chromosomes in a warp (idle lanes) so that
     // one chromosome may use up to a whole CTA's shared memory.
     int rc = -3;
     const int gmin = getenv("FFSGA_EVAL_G") ? atoi(getenv("FFSGA_EVAL_G")) : 0;  // experiments
-    if (I.maxM <= 4 && gmin <= 4 && (rc = eval_config_g<4>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
-    if (I.maxM <= 8 && (rc = eval_config_g<8>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
-    if (I.maxM <= 16 && (rc = eval_config_g<16>(I, sm_count, warps_cap, early, cfg)) != -1) return rc;
-    if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, warps_cap, early, cfg);
+    if (I.maxM <= 4 && gmin <= 4 && (rc = eval_config_g<4>(I, sm_count, warps_cap, cfg)) != -1) return rc;
+    if (I.maxM <= 8 && (rc = eval_config_g<8>(I, sm_count, warps_cap, cfg)) != -1) return rc;
+    if (I.maxM <= 16 && (rc = eval_config_g<16>(I, sm_count, warps_cap, cfg)) != -1) return rc;
+    if (I.maxM <= 32) return eval_config_g<32>(I, sm_count, warps_cap, cfg);
     return rc;
 }
 

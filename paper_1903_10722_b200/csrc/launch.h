@@ -77,14 +77,13 @@ struct WorkList {
 // ------------------------------------------------------------------ launchers
 struct EvalConfig {
     int G, warps, groups_per_cta, blocks_per_sm;
-    bool early;  // K1 pop order: this pop's loads before the previous pop's retire
+    int depth;   // K1 pops in flight (2, or 3 for large J)
     GroupLayout gl;
     BucketLayout bl;
     size_t smem;
 };
 // warps_cap: CTA size cap in warps (0 = 16); the CTA is also capped by shared memory.
-// early: pop loads issued before the previous pop's retire (best when one launch owns the GPU)
-int eval_config(const DevInst& I, int sm_count, int warps_cap, bool early, EvalConfig* cfg);
+int eval_config(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg);
 cudaError_t launch_eval(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,
                         int sm_count, bool schedule, cudaStream_t st);
 // random rows: item i seeded with seed_i = per_item ? derive_seed(base, first + i) : base and

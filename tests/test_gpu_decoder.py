@@ -53,7 +53,8 @@ def test_bad_gene_messages(capi, orc):
 
 
 SHAPES = [(20, 5, 3, 3), (6, 2, 2, 2), (100, 10, 2, 5), (100, 20, 2, 8), (500, 20, 2, 8), (37, 7, 1, 8),
-          (64, 3, 5, 16), (30, 4, 9, 32), (1, 2, 1, 2), (3, 2, 2, 2)]
+          (64, 3, 5, 16), (30, 4, 9, 32), (1, 2, 1, 2), (3, 2, 2, 2),
+          (1000, 20, 2, 8), (1500, 5, 2, 6)]  # J >= 1000: three pops in flight
 
 
 @pytest.mark.parametrize("J,S,lo,hi", SHAPES)
@@ -82,21 +83,21 @@ def test_integer_times_ties(capi, orc):
         assert np.array_equal(obj, eo) and np.array_equal(fit, ef)
 
 
-def test_ready_time_ties_redecoded_exactly(capi, orc):
+@pytest.mark.parametrize("J,S,M", [(30, 5, [3, 2, 3, 2, 3]), (1000, 4, [3, 2, 4, 2])])
+def test_ready_time_ties_redecoded_exactly(capi, orc, J, S, M):
     """The decoder pops by ready time alone and decodes a chromosome again in (ready, job) order
     when two consecutive pops tie.  Small integer times make ties occur in some chromosomes and
     not in others, so CTAs mix re-decoded and kept groups; every result must still be the
     reference's, bit for bit."""
     from pyoracle import InstanceData
     rng = np.random.default_rng(17)
-    J, S, M = 30, 5, [3, 2, 3, 2, 3]
     proc = rng.integers(1, 400, size=(J, sum(M))).astype(np.float64)
     release = rng.integers(0, 600, J).astype(np.float64)
     due = release + rng.integers(50, 400, J)
     d = InstanceData(J, S, M, proc, release, due, 1.0)
     oi = orc.instance(d)
     emax = oi.estimate_emax()
-    pop = oi.random_population(23, 0, 3000)
+    pop = oi.random_population(23, 0, 3000 if J < 100 else 300)
     obj, fit, mk, td = capi.Instance.from_data(d, emax).evaluate(pop, full=True)
     eo, ef, em, et = oi.score_batch(pop, emax)
     for a, b in ((obj, eo), (fit, ef), (mk, em), (td, et)):
@@ -112,8 +113,9 @@ def test_ready_time_ties_redecoded_exactly(capi, orc):
                 if len(np.unique(r)) < len(r):
                     return True
         return False
-    ties = sum(has_tie(g) for g in pop[:300])
-    assert 0 < ties < 300
+    if J < 100:
+        ties = sum(has_tie(g) for g in pop[:300])
+        assert 0 < ties < 300
 
 
 def test_decode_schedule_matches_reference(capi, orc):
