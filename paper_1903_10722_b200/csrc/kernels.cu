@@ -1526,6 +1526,22 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
     const long long cap = (long long)cfg.blocks_per_sm * sm_count;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    if (W.deal && I.algo != 1 && !schedule && blocks < sm_count) {
+        // A small launch that owns the GPU (one island, C1/C2): full CTAs would leave most SMs
+        // idle, so spread the items over up to one CTA per SM with fewer warps each -- a
+        // chromosome on a thinly filled SM decodes faster (less issue contention per pop).
+        constexpr int per_warp = 32 / G;
+        const long long want = (max_items + sm_count - 1) / sm_count;
+        const int gpc = (int)(((want + per_warp - 1) / per_warp) * per_warp);
+        if (gpc < cfg.groups_per_cta) {
+            EvalConfig c = cfg;
+            c.groups_per_cta = gpc;
+            c.warps = gpc / per_warp;
+            c.smem = (size_t)gpc * cfg.gl.bytes;
+            c.blocks_per_sm = 1;
+            return launch_eval_g<G>(I, c, W, max_items, sm_count, schedule, st);
+        }
+    }
     if (I.algo == 1) {
         if (schedule)
             k_eval_bkt<G, true><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.bl);
