@@ -43,15 +43,42 @@ SWEEP_N = 1 << 20
 
 
 def synthetic_machines(jobs, stages, lo=LO, hi=HI):
-    from paper_1903_10722_b200.islands import splitmix_next
+    """M[s] = lo + Rng(1000 + J*S).next_index(hi - lo + 1) (plain Python, so that
+    neither arm imports the other's code to build its config)."""
+    g, mask = 0x9E3779B97F4A7C15, (1 << 64) - 1
     st = 1000 + jobs * stages
     out = []
     for _ in range(stages):
-        st, u = splitmix_next(st)
-        unit = float(u >> 11) * 2.0 ** -53
-        v = int(unit * float(hi - lo + 1))
+        st = (st + g) & mask
+        z = st
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & mask
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & mask
+        u = z ^ (z >> 31)
+        v = int(float(u >> 11) * 2.0 ** -53 * float(hi - lo + 1))
         out.append(lo + min(v, hi - lo))
     return out
+
+
+def cpu_info():
+    """Host CPU model, current clock and thread count (nproc, CPU model, clocks)."""
+    model, mhz = None, []
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                k, _, v = line.partition(":")
+                k = k.strip()
+                if k == "model name" and model is None:
+                    model = v.strip()
+                elif k == "cpu MHz":
+                    mhz.append(float(v))
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "cpu_mhz_mean": (sum(mhz) / len(mhz)) if mhz else None,
+            "cpu_mhz_max": max(mhz) if mhz else None, "nproc": os.cpu_count(), "usable_threads": usable}
 
 
 def make_instance():
@@ -117,32 +144,58 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _ref_islands(ri, emax, derive):
+    """The 8 C3 islands on the reference (oracle/_ref): island i seed derive_seed(seed, i), even =
+    CellGrid 128x64, odd = PairPopulation 8192 (bench.py's island set, islands.py extension)."""
+    isl = []
+    for i in range(2 * COUPLES):
+        if i % 2 == 0:
+            isl.append(ri.cellular(emax, ISLAND_POP, derive(RUN_SEED, i), width=GRID[0], height=GRID[1]))
+        else:
+            isl.append(ri.pseudo(emax, ISLAND_POP, derive(RUN_SEED, i)))
+    return isl
+
+
+def _ref_island_objectives(isl):
+    """Per island: cellular objective at best_index, pseudo archive objective (the trace values,
+    solver.cpp:113,121)."""
+    out = []
+    for i, x in enumerate(isl):
+        if i % 2 == 0:
+            out.append(float(x.read()[1][x.best_index()]))
+        else:
+            out.append(float(x.archive()[2]))
+    return out
+
+
 def cpu_baseline_ga(inst_data, emax, workers):
-    """Reference CPU generation on a bounded sample: one couple (CellGrid 128x64 + PairPopulation
-    8192) of the 4, one generation each, workers = host threads; scaled to the 8-island step."""
+    """The reference's CPU generation (oracle/_ref: the unmodified reference sources) on the full
+    C3 island set, timed on this box's host cores: one warm-up generation, then 2 timed ones."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import RefLib, have_ref
     if not have_ref():
         return None
-    from paper_1903_10722_b200.islands import derive_seed
     ref = RefLib()
     ri = ref.instance(inst_data)
-    c = ri.cellular(emax, ISLAND_POP, derive_seed(RUN_SEED, 0), width=GRID[0], height=GRID[1])
-    p = ri.pseudo(emax, ISLAND_POP, derive_seed(RUN_SEED, 1))
-    c.step(workers)
-    p.step(workers)
-    t0 = time.perf_counter()
+    isl = _ref_islands(ri, emax, lambda b, k: int(ref.lib.ref_derive_seed(b, k)))
+    for x in isl:
+        x.step(workers)
     reps = 2
+    t0 = time.perf_counter()
     for _ in range(reps):
-        c.step(workers)
-        p.step(workers)
+        for x in isl:
+            x.step(workers)
     dt = (time.perf_counter() - t0) / reps
-    return {"value": 1.0 / (COUPLES * dt), "unit": "generations/s", "cores": workers, "kind": "reference",
-            "sample": f"{reps} generations of 1 of {COUPLES} couples (CellGrid 128x64 + PairPopulation 8192, "
-                      f"oracle/_ref, workers={workers}), time x{COUPLES}"}
+    out = {"value": 1.0 / dt, "unit": "generations/s", "cores": workers, "kind": "reference",
+           "sample": f"{reps} timed generations (after 1 warm-up) of the full C3 island set: 4 CellGrid 128x64 + "
+                     f"4 PairPopulation 8192 steps, oracle/_ref, workers={workers}"}
+    out.update(cpu_info())
+    return out
 
 
 def reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref) -- nothing of the product package is
+    imported here."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
@@ -151,14 +204,13 @@ def reference_arm(args):
     if not have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libffsga_ref.so not built"}))
         return 0
-    from pyoracle import InstanceData
-    from paper_1903_10722_b200.islands import derive_seed
     workers = os.cpu_count() or 1
     ref = RefLib()
     m = synthetic_machines(J, S)
     data = ref.generate(J, S, m, weight=WEIGHT, seed=GEN_SEED)
     ri = ref.instance(data)
     emax = ri.estimate_emax()
+    extra = {}
     if args.workload == "decoder":
         n = 20000
         pop = ri.random_population(99, 0, n)
@@ -173,12 +225,7 @@ def reference_arm(args):
         sample = f"{n} chromosomes per step (of the 1M launch), Evaluator::score via parallel_chunks"
         cfg = {"workload": "C5 decoder sweep 500x20, M in [2,8]", "n_per_step_sampled": n}
     else:
-        isl = []
-        for i in range(2 * COUPLES):
-            if i % 2 == 0:
-                isl.append(ri.cellular(emax, ISLAND_POP, derive_seed(RUN_SEED, i), width=GRID[0], height=GRID[1]))
-            else:
-                isl.append(ri.pseudo(emax, ISLAND_POP, derive_seed(RUN_SEED, i)))
+        isl = _ref_islands(ri, emax, lambda b, k: int(ref.lib.ref_derive_seed(b, k)))
         for _ in range(args.warmup):
             for x in isl:
                 x.step(workers)
@@ -191,25 +238,59 @@ def reference_arm(args):
         unit = "generations/s"
         sample = (f"full C3 generation per step: 4 CellGrid 128x64 + 4 PairPopulation 8192 steps, "
                   f"workers={workers}")
-        cfg = ga_config(world)
-    print(json.dumps({
+        cfg = ga_config(world, m)
+        extra["island_best_objectives"] = _ref_island_objectives(isl)
+        extra["generations_done"] = args.warmup + args.steps
+    cpu = {"value": val, "unit": unit, "cores": workers, "kind": "reference", "sample": sample}
+    cpu.update(cpu_info())
+    line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": cfg,
-        "cpu_baseline": {"value": val, "unit": unit, "cores": workers, "kind": "reference", "sample": sample},
+        "data": "synthetic", "config": cfg, "cpu_baseline": cpu,
         "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }
+    line.update(extra)
+    print(json.dumps(line), flush=True)
     return 0
 
 
-def ga_config(world):
+def ga_config(world, machines):
     return {"workload": "C3: FFS 500 jobs x 20 stages x 2-8 machines/stage, 8 islands (4 cellular 128x64 + "
                         "4 pseudo 8192), pop 65536",
-            "jobs": J, "stages": S, "machines": synthetic_machines(J, S), "islands": 2 * COUPLES,
+            "jobs": J, "stages": S, "machines": list(machines), "islands": 2 * COUPLES,
             "population": 2 * COUPLES * ISLAND_POP, "gap": GAP, "theta": THETA, "seed": RUN_SEED,
             "ranks": world, "islands_per_rank": 2 * COUPLES // world if world <= 2 * COUPLES else None,
             "l2": "inputs larger than L2 (resident population 0.77 GB > 126 MB)"}
+
+
+PROFILE = os.path.join(ROOT, "profiles", "r2_k1_profile.json")
+
+
+def load_profile():
+    """The committed ncu numbers of this library's K1 inside the C3 step (profiles/r2_k1_profile.json,
+    written by profiles/tools/summarize_ncu.py from an `ncu --set full` capture of bench.py)."""
+    try:
+        with open(PROFILE) as f:
+            d = json.load(f)
+        d["source"] = os.path.relpath(PROFILE, ROOT)
+        return d
+    except Exception:
+        return {}
+
+
+def island_objectives(model, comm):
+    """Per island (global order): cellular objective at best_index, pseudo archive objective --
+    the reference arm prints the same list for the same generations."""
+    n = model.cfg.n_islands
+    vec = np.full(n, np.nan)
+    for i, isl in model.local.items():
+        vec[i] = isl.best()[2] if model.cfg.kind(i) == "cellular" else isl.archive()[2]
+    if comm is not None:
+        from paper_1903_10722_b200.islands import owner
+        allv = comm.allgather(vec)
+        vec = np.array([allv[owner(i, n, comm.world), i] for i in range(n)])
+    return [float(x) for x in vec]
 
 
 def sweep_traffic(n):
@@ -311,6 +392,8 @@ def main():
         l1 = capi.launch_count()
         evals = model.inst.evaluations() - ev0
         eval_ms, eval_n = model.inst.timing(0)
+        eval_busy_ms = model.inst.timing_busy(0)
+        island_obj = island_objectives(model, comm)
         breed_ms, _ = model.inst.timing(1)
         commit_ms, _ = model.inst.timing(2)
         model.inst.set_timing(False)
@@ -323,27 +406,19 @@ def main():
             ms_max, evals_all = dev_ms, float(evals)
         gens_per_s = args.steps / (ms_max / 1e3)
         algo_bytes = evals * (L + 16)
+        prof = load_profile()
         traffic = None  # DRAM bytes per K1 launch from the committed ncu capture, scaled per evaluation
-        try:
-            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-                tr = json.load(f)
-            traffic = tr["traffic_bytes_per_eval"] * (evals / max(1, eval_n))
-        except Exception:
-            pass
-        achieved = algo_bytes / (eval_ms / 1e3) / 1e9 if eval_ms > 0 else 0.0
-        issue = None  # K1 is issue/latency bound: the integer-issue roofline from the same capture
-        try:
-            with open(os.path.join(ROOT, "profiles", "r1_ncu.json")) as f:
-                for k in json.load(f)["kernels"]:
-                    if "k_eval<8, 0" in k["kernel"]:
-                        ia = k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0
-                        issue = {"bound": "issue", "frac": ia, "unit": "warp instructions/cycle/SMSP",
-                                 "achieved": ia, "peak": 1.0,
-                                 "warps_per_sm": k["sm__warps_active.avg.per_cycle_active"],
-                                 "source": "profiles/r1_ncu.json (ncu --set full of this step's K1 launch)"}
-                        break
-        except Exception:
-            pass
+        if prof.get("traffic_bytes_per_eval"):
+            traffic = prof["traffic_bytes_per_eval"] * (evals / max(1, eval_n))
+        # K1 of the cellular and the pseudo chain run concurrently on two streams: the kernel's
+        # time is the union of its launch intervals (timing_busy), not the per-stream sum
+        achieved = algo_bytes / (eval_busy_ms / 1e3) / 1e9 if eval_busy_ms > 0 else 0.0
+        issue = None  # K1 is issue/latency bound: the issue roofline from the committed capture
+        if prof.get("issue_active") is not None:
+            issue = {"bound": "issue", "frac": prof["issue_active"], "unit": "warp instructions/cycle/SMSP",
+                     "achieved": prof["issue_active"], "peak": 1.0, "warps_per_sm": prof.get("warps_per_sm"),
+                     "threads_per_inst": prof.get("threads_per_inst"), "kernel": prof.get("kernel"),
+                     "source": prof.get("source")}
 
         # e2e: the public API call a user makes (instance upload, island init, K generations,
         # traces + champion back to the host), wall clock; median of E2E_RUNS independent runs
@@ -374,7 +449,8 @@ def main():
         e2e_s = runs[len(runs) // 2][0]
         e2e_parts = {"instance_and_init_s": runs[len(runs) // 2][1], "run_s": runs[len(runs) // 2][2],
                      "run_device_s": runs[len(runs) // 2][3], "runs_total_s": [r[0] for r in runs]}
-        h2d = (L * sum(synthetic_machines(J, S)) + 2 * J) * 8 + S * 4
+        # instance upload: proc (J x sum M fp64) + release + due (fp64) + machines per stage (int32)
+        h2d = J * sum(synthetic_machines(J, S)) * 8 + 16 * J + 4 * S
         d2h = 2 * COUPLES * args.steps * 8 + L * 4 + 5 * 8
 
         sweep = None
@@ -391,16 +467,21 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (SURVEY 8(d) generator convention, random-init populations)",
-                "config": ga_config(world),
+                "config": ga_config(world, synthetic_machines(J, S)),
                 "evals_per_s": evals_all / (ms_max / 1e3),
                 "evals_per_step": evals_all / args.steps,
-                "kernel_ms_per_step": {"eval": eval_ms / args.steps, "breed": breed_ms / args.steps,
-                                       "commit": commit_ms / args.steps,
-                                       "note": "summed per stream; the cellular and pseudo chains overlap"},
+                "kernel_ms_per_step": {"eval": eval_ms / args.steps, "eval_busy": eval_busy_ms / args.steps,
+                                       "breed": breed_ms / args.steps, "commit": commit_ms / args.steps,
+                                       "note": "eval/breed/commit summed per stream (the cellular and pseudo "
+                                               "chains overlap); eval_busy = union of the K1 intervals"},
+                "island_best_objectives": island_obj,
+                "generations_done": args.warmup + args.steps,
                 "roofline": {"bound": "hbm", "kernel": "k_eval (K1 decoder)", "achieved": achieved,
                              "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                              "frac": achieved / hbm_peak, "traffic": traffic,
-                             "traffic_unit": "bytes per launch (ncu dram read+write, profiles/r1_traffic.json)",
+                             "traffic_unit": "bytes per launch (ncu dram read+write, %s)" % prof.get("source"),
+                             "time_basis": "union of the K1 launch intervals (CUDA events on both step streams)",
+                             "launches": eval_n,
                              "algorithmic_bytes_per_launch": algo_bytes / max(1, eval_n),
                              "algorithmic_bytes_per_eval": L + 16,
                              "issue_roofline": issue,

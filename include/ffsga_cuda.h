@@ -190,12 +190,36 @@ int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits
 int ffsga_cuda_pseudo_import(ffsga_cuda_pseudo p, int k, const int32_t* genes, const double* fitness,
                              const double* objective);
 
+/* Device-resident halves (the data plane between GPUs: the packet is device memory that NCCL or
+ * a peer copy moves over NVLink; nothing is staged through the host).  A migrant packet is
+ * [fitness[k] f64][objective[k] f64][payload]: payload = k stage-major gene rows (from a
+ * cellular island) or k packed bit chromosomes of ceil(total_bits/64) u64 words, LSB-first
+ * (from a pseudo island).  Export and import are ordered on `stream` (a cudaStream_t; NULL =
+ * the legacy default stream) and never synchronise the host.  A cellular island imports a
+ * pseudo island's packet and vice versa; best lands on worst, and a pseudo import feeds the
+ * archive in install order (migration.cpp:47-69, pseudo.cpp:98-113). */
+int ffsga_cuda_packet_bytes(ffsga_cuda_instance inst, int from_kind /* 0 cellular, 1 pseudo */, int k,
+                            int64_t* bytes);
+int ffsga_cuda_cellular_export_device(ffsga_cuda_cellular c, int k, void* packet, void* stream);
+int ffsga_cuda_pseudo_export_device(ffsga_cuda_pseudo p, int k, void* packet, void* stream);
+int ffsga_cuda_cellular_import_device(ffsga_cuda_cellular c, int k, const void* packet, void* stream);
+int ffsga_cuda_pseudo_import_device(ffsga_cuda_pseudo p, int k, const void* packet, void* stream);
+/* island statistics into device memory, ordered on `stream`: out4 = {best fitness, best
+ * objective, archive fitness, archive objective} (best_index of cellular.cpp:184-189 /
+ * pseudo.cpp:91-96; archive of pseudo.hpp:78-80, -1 / 0 for a cellular island) -- what the
+ * rendezvous policy (solver.cpp:142-163) and the champion rule (solver.cpp:175-183) read */
+int ffsga_cuda_cellular_state_device(ffsga_cuda_cellular c, double* out4, void* stream);
+int ffsga_cuda_pseudo_state_device(ffsga_cuda_pseudo p, double* out4, void* stream);
+
 /* ---- measurement ------------------------------------------------------------------------------
  * Per-kernel CUDA-event timing on the launching stream (off by default).  When enabled, every
  * k_eval launch of a batch or of ffsga_cuda_step is bracketed by events; totals accumulate. */
 int ffsga_cuda_set_timing(ffsga_cuda_instance inst, int enabled);
 /* total milliseconds and launch count of: 0 = K1 eval, 1 = K3+K4 breed, 2 = K6 commit */
 int ffsga_cuda_timing(ffsga_cuda_instance inst, int which, double* ms, int64_t* launches);
+/* milliseconds during which at least one launch of that kind was running: the union of the
+ * event intervals, so the concurrent cellular and pseudo chains of a joint step count once */
+int ffsga_cuda_timing_busy(ffsga_cuda_instance inst, int which, double* busy_ms);
 int ffsga_cuda_reset_timing(ffsga_cuda_instance inst);
 /* makespan evaluations performed by ffsga_cuda_step on this instance since creation
  * (cellular children + crossed pseudo members; device counter) */

@@ -90,10 +90,18 @@ _SIGS = {
     "ffsga_cuda_pseudo_export": (_i32, [_vp, _i32, _pu8, _pd, _pd]),
     "ffsga_cuda_cellular_import": (_i32, [_vp, _i32, _pu8, _pd, _pd]),
     "ffsga_cuda_pseudo_import": (_i32, [_vp, _i32, _pi32, _pd, _pd]),
+    "ffsga_cuda_packet_bytes": (_i32, [_vp, _i32, _i32, C.POINTER(_i64)]),
+    "ffsga_cuda_cellular_export_device": (_i32, [_vp, _i32, _vp, _vp]),
+    "ffsga_cuda_pseudo_export_device": (_i32, [_vp, _i32, _vp, _vp]),
+    "ffsga_cuda_cellular_import_device": (_i32, [_vp, _i32, _vp, _vp]),
+    "ffsga_cuda_pseudo_import_device": (_i32, [_vp, _i32, _vp, _vp]),
+    "ffsga_cuda_cellular_state_device": (_i32, [_vp, _vp, _vp]),
+    "ffsga_cuda_pseudo_state_device": (_i32, [_vp, _vp, _vp]),
     "ffsga_cuda_last_step_ms": (_i32, [_vp, C.POINTER(C.c_float)]),
     "ffsga_cuda_evaluations": (_i32, [_vp, C.POINTER(_i64)]),
     "ffsga_cuda_set_timing": (_i32, [_vp, _i32]),
     "ffsga_cuda_timing": (_i32, [_vp, _i32, _pd, C.POINTER(_i64)]),
+    "ffsga_cuda_timing_busy": (_i32, [_vp, _i32, _pd]),
     "ffsga_cuda_reset_timing": (_i32, [_vp]),
     "ffsga_cuda_launch_count": (_i32, [C.POINTER(_i64)]),
 }
@@ -154,6 +162,7 @@ class Instance:
         release = np.ascontiguousarray(release, dtype=np.float64)
         due = np.ascontiguousarray(due, dtype=np.float64)
         self.emax = float(emax)
+        self.device = int(device)
         h = C.c_void_p()
         _check(lib().ffsga_cuda_instance_create(device, self.num_jobs, self.num_stages, _p(self.machines, _pi32),
                                                 _p(proc, _pd), _p(release, _pd), _p(due, _pd), float(weight),
@@ -219,6 +228,12 @@ class Instance:
         rep = dict(makespan=r[0], total_tardiness=r[1], objective=r[2], fitness=r[3], emax_used=r[4])
         return m, s, c, rep
 
+    def packet_bytes(self, from_kind, k):
+        """Bytes of a migrant packet of k members leaving a cellular (0) or pseudo (1) island."""
+        n = C.c_int64()
+        _check(lib().ffsga_cuda_packet_bytes(self.h, int(from_kind), int(k), C.byref(n)))
+        return n.value
+
     def last_step_ms(self):
         ms = C.c_float()
         _check(lib().ffsga_cuda_last_step_ms(self.h, C.byref(ms)))
@@ -234,6 +249,12 @@ class Instance:
 
     def reset_timing(self):
         _check(lib().ffsga_cuda_reset_timing(self.h))
+
+    def timing_busy(self, which):
+        """Milliseconds during which at least one launch of kind `which` ran (interval union)."""
+        ms = C.c_double()
+        _check(lib().ffsga_cuda_timing_busy(self.h, which, C.byref(ms)))
+        return ms.value
 
     def timing(self, which):
         ms, n = C.c_double(), C.c_int64()
@@ -376,6 +397,19 @@ class Cellular:
         o = np.ascontiguousarray(obj, dtype=np.float64)
         _check(lib().ffsga_cuda_cellular_import(self.h, len(f), _p(b, _pu8), _p(f, _pd), _p(o, _pd)))
 
+    # -- device-resident data plane (torch CUDA tensors; ordered on torch's current stream)
+    def export_packet(self, k, out=None):
+        """k best cells as a device migrant packet (uint8 torch tensor on this island's GPU)."""
+        return _export_packet(self, 0, lib().ffsga_cuda_cellular_export_device, k, out)
+
+    def import_packet(self, packet, k):
+        """Install a pseudo island's packet over the k worst cells (device to device)."""
+        _import_packet(self, lib().ffsga_cuda_cellular_import_device, packet, k)
+
+    def state_device(self, out):
+        """{best fitness, best objective, -1, 0} into a float64 CUDA tensor of 4 (device copy)."""
+        _state_device(self, lib().ffsga_cuda_cellular_state_device, out)
+
 
 class Pseudo:
     """Device complementary-pair island (ffsga_cuda_pseudo ~ PairPopulation)."""
@@ -452,6 +486,49 @@ class Pseudo:
         f = np.ascontiguousarray(fit, dtype=np.float64)
         o = np.ascontiguousarray(obj, dtype=np.float64)
         _check(lib().ffsga_cuda_pseudo_import(self.h, len(f), _p(g, _pi32), _p(f, _pd), _p(o, _pd)))
+
+    # -- device-resident data plane (torch CUDA tensors; ordered on torch's current stream)
+    def export_packet(self, k, out=None):
+        """k best members as a device migrant packet (uint8 torch tensor on this island's GPU)."""
+        return _export_packet(self, 1, lib().ffsga_cuda_pseudo_export_device, k, out)
+
+    def import_packet(self, packet, k):
+        """Install a cellular island's packet over the k worst members; the archive absorbs them."""
+        _import_packet(self, lib().ffsga_cuda_pseudo_import_device, packet, k)
+
+    def state_device(self, out):
+        """{best fitness, best objective, archive fitness, archive objective} into a float64 CUDA
+        tensor of 4 (device copy)."""
+        _state_device(self, lib().ffsga_cuda_pseudo_state_device, out)
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _export_packet(isl, kind, fn, k, out):
+    import torch
+    nbytes = isl.inst.packet_bytes(kind, k)
+    if out is None:
+        out = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=torch.device("cuda", isl.inst.device))
+    if out.numel() < nbytes or not out.is_cuda or not out.is_contiguous():
+        raise ValueError("export_packet: out must be a contiguous CUDA uint8 tensor of packet_bytes()")
+    _check(fn(isl.h, int(k), C.c_void_p(out.data_ptr()), _stream()))
+    return out
+
+
+def _import_packet(isl, fn, packet, k):
+    if not packet.is_cuda or not packet.is_contiguous():
+        raise ValueError("import_packet: packet must be a contiguous CUDA tensor")
+    _check(fn(isl.h, int(k), C.c_void_p(packet.data_ptr()), _stream()))
+
+
+def _state_device(isl, fn, out):
+    import torch
+    if not out.is_cuda or out.dtype != torch.float64 or out.numel() < 4 or not out.is_contiguous():
+        raise ValueError("state_device: out must be a contiguous float64 CUDA tensor of >= 4 elements")
+    _check(fn(isl.h, C.c_void_p(out.data_ptr()), _stream()))
 
 
 def step(cells=(), pseudos=(), generations=1, traces=True):

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -178,6 +179,7 @@ struct ffsga_cuda_instance_t {
     // timing: event pairs recorded around launches, resolved lazily (no sync in the timed path)
     bool timing = false;
     double t_ms[3] = {0, 0, 0};
+    double t_busy[3] = {0, 0, 0};  // union of the launch intervals (concurrent streams counted once)
     long long t_n[3] = {0, 0, 0};
     struct Pending {
         int which;
@@ -237,12 +239,37 @@ struct ffsga_cuda_instance_t {
         pending.push_back(p);
     }
     void resolve_timing() {
+        // intervals relative to the first pending start (offsets may be negative: the launches
+        // of concurrent streams are recorded in host order, not device order)
+        std::vector<std::pair<float, float>> iv[3];
         for (auto& p : pending) {
             CK(cudaEventSynchronize(p.b));
-            float ms = 0;
+            float ms = 0, at = 0;
             CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            CK(cudaEventElapsedTime(&at, pending.front().a, p.a));
             t_ms[p.which] += ms;
             t_n[p.which] += 1;
+            iv[p.which].push_back({at, at + ms});
+        }
+        for (int w = 0; w < 3; ++w) {
+            std::sort(iv[w].begin(), iv[w].end());
+            double busy = 0;
+            float lo = 0, hi = 0;
+            bool open = false;
+            for (auto& x : iv[w]) {
+                if (open && x.first <= hi) {
+                    hi = std::max(hi, x.second);
+                    continue;
+                }
+                if (open) busy += hi - lo;
+                lo = x.first;
+                hi = x.second;
+                open = true;
+            }
+            if (open) busy += hi - lo;
+            t_busy[w] += busy;
+        }
+        for (auto& p : pending) {
             pool.push_back(p.a);
             pool.push_back(p.b);
         }
@@ -659,6 +686,7 @@ void batch_upload(ffsga_cuda_batch b, const T* genes, int64_t n) {
     if (!b || !genes) fail(FFSGA_ERR_ARG, "batch_upload: null pointer");
     if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_upload: n exceeds capacity");
     auto* I = b->inst;
+    std::lock_guard<std::mutex> lk(I->mu);  // the instance stream may be capturing a step graph
     I->use();
     const long long L = (long long)I->J * I->S;
     const long long chunk = std::min<long long>(std::max<long long>(n, 1), 1 << 14);
@@ -683,6 +711,7 @@ int ffsga_cuda_batch_create(ffsga_cuda_instance inst, int64_t capacity, ffsga_cu
     return guard([&] {
         if (!inst || !out) fail(FFSGA_ERR_ARG, "batch_create: null pointer");
         if (capacity < 1) fail(FFSGA_ERR_CONTRACT, "batch capacity must be >= 1");
+        std::lock_guard<std::mutex> lk(inst->mu);
         inst->use();
         auto* b = new ffsga_cuda_batch_t();
         std::unique_ptr<ffsga_cuda_batch_t> hold(b);
@@ -711,6 +740,7 @@ int ffsga_cuda_batch_fill_random(ffsga_cuda_batch b, uint64_t base_seed, int64_t
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
         if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_fill_random: n exceeds capacity");
         auto* I = b->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
         I->use();
         CK(launch_random_rows(I->d, b->rows.as<uint8_t>(), (long long)I->block(), n, base_seed, first, true, I->stream));
         g_launches += 1;
@@ -730,6 +760,7 @@ int ffsga_cuda_batch_evaluate(ffsga_cuda_batch b, int64_t n) {
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
         if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_evaluate: n exceeds capacity");
         auto* I = b->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
         I->use();
         EvalItems W{};
         W.n = n;
@@ -762,6 +793,7 @@ int ffsga_cuda_batch_results(ffsga_cuda_batch b, int64_t n, double* obj, double*
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
         if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_results: n exceeds capacity");
         auto* I = b->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
         I->use();
         const size_t bytes = sizeof(double) * n;
         if (obj) CK(cudaMemcpyAsync(obj, b->obj.p, bytes, cudaMemcpyDeviceToHost, I->stream));
@@ -791,6 +823,7 @@ int ffsga_cuda_batch_download(ffsga_cuda_batch b, int64_t first, int64_t n, int3
         if (!b || !genes) fail(FFSGA_ERR_ARG, "null pointer");
         if (first < 0 || n < 0 || first + n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_download: range");
         auto* I = b->inst;
+        std::lock_guard<std::mutex> lk(I->mu);
         I->use();
         const size_t L = (size_t)I->J * I->S;
         DevBuf out;
@@ -806,6 +839,7 @@ int ffsga_cuda_batch_download(ffsga_cuda_batch b, int64_t first, int64_t n, int3
 int ffsga_cuda_batch_sync(ffsga_cuda_batch b) {
     return guard([&] {
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
+        std::lock_guard<std::mutex> lk(b->inst->mu);
         b->inst->use();
         CK(cudaStreamSynchronize(b->inst->stream));
     });
@@ -1507,11 +1541,17 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             // the generation sequence is launch-bound for small islands: capture a chunk of
             // generations once (device-side generation counters make it replayable)
             const int chunk = std::min(generations, 16);
-            const std::vector<const void*> key = {cdev, pdev, (const void*)ptrs, (const void*)wobj,
-                                                  I->wl_count.p, (const void*)groups.size(),
-                                                  (const void*)(intptr_t)nc, (const void*)(intptr_t)np,
-                                                  (const void*)(intptr_t)n_cells, (const void*)(intptr_t)n_pairs,
-                                                  (const void*)(intptr_t)chunk};
+            // the captured launches bake in every group's island range, unit counts (grid sizes)
+            // and work-list offset, so all of them are part of the key
+            std::vector<const void*> key = {cdev, pdev, (const void*)ptrs, (const void*)wobj,
+                                            I->wl_count.p, (const void*)groups.size(),
+                                            (const void*)(intptr_t)nc, (const void*)(intptr_t)np,
+                                            (const void*)(intptr_t)n_cells, (const void*)(intptr_t)n_pairs,
+                                            (const void*)(intptr_t)chunk};
+            for (const Group& G : groups)
+                for (long long v : {(long long)G.c0, (long long)G.c1, (long long)G.p0, (long long)G.p1, G.cells,
+                                    G.pairs, G.item0})
+                    key.push_back((const void*)(intptr_t)v);
             if (!I->graph_exec || I->graph_key != key) {
                 if (I->graph_exec) {
                     CK(cudaGraphExecDestroy(I->graph_exec));
@@ -1615,64 +1655,210 @@ int ffsga_cuda_migrate_pseudo_to_cellular(ffsga_cuda_pseudo from, ffsga_cuda_cel
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// ---- migrant packets: [fit[k] fp64][obj[k] fp64][payload] (kernels.cu "Migrant packets")
+size_t packet_bytes(const ffsga_cuda_instance_t* I, int from_kind, int k) {
+    const size_t payload = from_kind == 0 ? I->block() : sizeof(unsigned long long) * (size_t)I->words;
+    return (size_t)k * (2 * sizeof(double) + payload);
+}
+
+// Every packet routine runs on the instance stream under I->mu, ordered after the caller's
+// stream (fork) and before the caller's later work (join): no host synchronisation.
+struct Ordered {
+    ffsga_cuda_instance_t* I;
+    cudaStream_t user;
+    Ordered(ffsga_cuda_instance_t* I_, void* stream) : I(I_), user(static_cast<cudaStream_t>(stream)) {
+        CK(cudaEventRecord(I->fork, user));
+        CK(cudaStreamWaitEvent(I->stream, I->fork, 0));
+    }
+    void done() {
+        CK(cudaEventRecord(I->join, I->stream));
+        CK(cudaStreamWaitEvent(user, I->join, 0));
+    }
+};
+
+void export_cell_packet(ffsga_cuda_cellular_t* c, int k, unsigned char* packet) {
+    ffsga_cuda_instance_t* I = c->inst;
+    const int q = c->parity();
+    sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_a);
+    CK(launch_export_cell(I->d, c->d, I->mg_idx_a.as<long long>(), k, q, packet + 2 * sizeof(double) * k,
+                          reinterpret_cast<double*>(packet), I->stream));
+    g_launches += 1;
+}
+
+void export_pseudo_packet(ffsga_cuda_pseudo_t* p, int k, unsigned char* packet) {
+    ffsga_cuda_instance_t* I = p->inst;
+    sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_a);
+    CK(launch_export_pseudo(I->d, p->d, I->mg_idx_a.as<long long>(), k,
+                            reinterpret_cast<unsigned long long*>(packet + 2 * sizeof(double) * k),
+                            reinterpret_cast<double*>(packet), I->stream));
+    g_launches += 1;
+}
+
+// a pseudo island's packet installed over the k worst cells (migration.cpp:59-69)
+void import_into_cell(ffsga_cuda_cellular_t* c, int k, const unsigned char* packet) {
+    ffsga_cuda_instance_t* I = c->inst;
+    const int q = c->parity();
+    sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_b);
+    CK(launch_migrate_p2c(I->d, PseudoIsland{}, c->d, nullptr, I->mg_idx_b.as<long long>(), k, q, I->stream,
+                          reinterpret_cast<const unsigned long long*>(packet + 2 * sizeof(double) * k),
+                          reinterpret_cast<const double*>(packet)));
+    g_launches += 1;
+    refresh_stats(c, nullptr, 0);
+}
+
+// a cellular island's packet installed over the k worst members; the archive absorbs them
+// (migration.cpp:47-57, pseudo.cpp:98-113)
+void import_into_pseudo(ffsga_cuda_pseudo_t* p, int k, const unsigned char* packet) {
+    ffsga_cuda_instance_t* I = p->inst;
+    sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_b);
+    CK(launch_migrate_c2p(I->d, CellIsland{}, p->d, nullptr, I->mg_idx_b.as<long long>(), k, 0,
+                          I->dBitStage.as<uint16_t>(), I->stream, packet + 2 * sizeof(double) * k,
+                          reinterpret_cast<const double*>(packet)));
+    g_launches += 2;
+    refresh_stats(nullptr, p, 0);
+}
+
+void check_migrants(int k, int n, const void* ptr) {
+    if (k < 0 || k > n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+    if (k > 0 && !ptr) fail(FFSGA_ERR_ARG, "migrant packet: null pointer");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffsga_cuda_packet_bytes(ffsga_cuda_instance inst, int from_kind, int k, int64_t* bytes) {
+    return guard([&] {
+        if (!inst || !bytes || (from_kind != 0 && from_kind != 1) || k < 0) fail(FFSGA_ERR_ARG, "packet_bytes: bad argument");
+        *bytes = (int64_t)packet_bytes(inst, from_kind, k);
+    });
+}
+
+int ffsga_cuda_cellular_export_device(ffsga_cuda_cellular c, int k, void* packet, void* stream) {
+    return guard([&] {
+        if (!c) fail(FFSGA_ERR_ARG, "export: null island");
+        check_migrants(k, c->n, packet);
+        if (k == 0) return;
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        c->inst->use();
+        Ordered o(c->inst, stream);
+        export_cell_packet(c, k, static_cast<unsigned char*>(packet));
+        o.done();
+    });
+}
+
+int ffsga_cuda_pseudo_export_device(ffsga_cuda_pseudo p, int k, void* packet, void* stream) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "export: null island");
+        check_migrants(k, p->n, packet);
+        if (k == 0) return;
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        p->inst->use();
+        Ordered o(p->inst, stream);
+        export_pseudo_packet(p, k, static_cast<unsigned char*>(packet));
+        o.done();
+    });
+}
+
+int ffsga_cuda_cellular_import_device(ffsga_cuda_cellular c, int k, const void* packet, void* stream) {
+    return guard([&] {
+        if (!c) fail(FFSGA_ERR_ARG, "import: null island");
+        check_migrants(k, c->n, packet);
+        if (k == 0) return;
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        c->inst->use();
+        Ordered o(c->inst, stream);
+        import_into_cell(c, k, static_cast<const unsigned char*>(packet));
+        o.done();
+    });
+}
+
+int ffsga_cuda_pseudo_import_device(ffsga_cuda_pseudo p, int k, const void* packet, void* stream) {
+    return guard([&] {
+        if (!p) fail(FFSGA_ERR_ARG, "import: null island");
+        check_migrants(k, p->n, packet);
+        if (k == 0) return;
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        p->inst->use();
+        Ordered o(p->inst, stream);
+        import_into_pseudo(p, k, static_cast<const unsigned char*>(packet));
+        o.done();
+    });
+}
+
+int ffsga_cuda_cellular_state_device(ffsga_cuda_cellular c, double* out4, void* stream) {
+    return guard([&] {
+        if (!c || !out4) fail(FFSGA_ERR_ARG, "state_device: null pointer");
+        std::lock_guard<std::mutex> lk(c->inst->mu);
+        c->inst->use();
+        Ordered o(c->inst, stream);
+        CK(cudaMemcpyAsync(out4, reinterpret_cast<const char*>(c->st.p) + offsetof(IslandState, best_fit),
+                           4 * sizeof(double), cudaMemcpyDeviceToDevice, c->inst->stream));
+        o.done();
+    });
+}
+
+int ffsga_cuda_pseudo_state_device(ffsga_cuda_pseudo p, double* out4, void* stream) {
+    return guard([&] {
+        if (!p || !out4) fail(FFSGA_ERR_ARG, "state_device: null pointer");
+        std::lock_guard<std::mutex> lk(p->inst->mu);
+        p->inst->use();
+        Ordered o(p->inst, stream);
+        CK(cudaMemcpyAsync(out4, reinterpret_cast<const char*>(p->st.p) + offsetof(IslandState, best_fit),
+                           4 * sizeof(double), cudaMemcpyDeviceToDevice, p->inst->stream));
+        o.done();
+    });
+}
+
+// ---- host-buffer export/import: the same packets, staged through host memory
 int ffsga_cuda_cellular_export(ffsga_cuda_cellular c, int k, int32_t* genes, double* fit, double* obj) {
     return guard([&] {
         if (!c || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
-        if (k < 0 || k > c->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        check_migrants(k, c->n, genes);
         if (k == 0) return;
         ffsga_cuda_instance_t* I = c->inst;
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
-        const int q = c->parity();
-        sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_a);
-        std::vector<long long> best(k);
-        CK(cudaMemcpyAsync(best.data(), I->mg_idx_a.p, sizeof(long long) * k, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaStreamSynchronize(I->stream));
-        std::vector<long long> storage = cell_storage_index(c);
-        std::vector<long long> src(k);
-        for (int i = 0; i < k; ++i) src[i] = storage[best[i]];
-        DevBuf dsrc, out;
-        upload(dsrc, src);
+        DevBuf pk, out;
+        pk.alloc(packet_bytes(I, 0, k));
+        export_cell_packet(c, k, pk.as<unsigned char>());
         const size_t L = (size_t)I->J * I->S;
         out.alloc(sizeof(int32_t) * L * k);
-        CK(launch_rows_to_int(I->d, c->genes.as<uint8_t>(), (long long)I->block(), dsrc.as<long long>(), out.as<int32_t>(), k,
-                              I->stream));
+        CK(launch_rows_to_int(I->d, pk.as<uint8_t>() + 2 * sizeof(double) * k, (long long)I->block(), nullptr,
+                              out.as<int32_t>(), k, I->stream));
         g_launches += 1;
         CK(cudaMemcpyAsync(genes, out.p, sizeof(int32_t) * L * k, cudaMemcpyDeviceToHost, I->stream));
-        std::vector<double> f(c->n), o(c->n);
-        CK(cudaMemcpyAsync(f.data(), c->fit.as<double>() + (size_t)q * c->n, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaMemcpyAsync(o.data(), c->obj.as<double>() + (size_t)q * c->n, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(fit, pk.p, sizeof(double) * k, cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(obj, pk.as<double>() + k, sizeof(double) * k, cudaMemcpyDeviceToHost, I->stream));
         CK(cudaStreamSynchronize(I->stream));
-        for (int i = 0; i < k; ++i) {
-            fit[i] = f[best[i]];
-            obj[i] = o[best[i]];
-        }
     });
 }
 
 int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* fit, double* obj) {
     return guard([&] {
         if (!p || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
-        if (k < 0 || k > p->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        check_migrants(k, p->n, bits);
         if (k == 0) return;
         ffsga_cuda_instance_t* I = p->inst;
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
-        sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_a);
-        std::vector<long long> best(k);
-        CK(cudaMemcpyAsync(best.data(), I->mg_idx_a.p, sizeof(long long) * k, cudaMemcpyDeviceToHost, I->stream));
-        std::vector<double> f(p->n), o(p->n);
-        CK(cudaMemcpyAsync(f.data(), p->fit.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaMemcpyAsync(o.data(), p->obj.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
+        DevBuf pk;
+        const size_t bytes = packet_bytes(I, 1, k);
+        pk.alloc(bytes);
+        export_pseudo_packet(p, k, pk.as<unsigned char>());
+        std::vector<unsigned char> host(bytes);
+        CK(cudaMemcpyAsync(host.data(), pk.p, bytes, cudaMemcpyDeviceToHost, I->stream));  // one copy
         CK(cudaStreamSynchronize(I->stream));
-        const int W = I->words, nb = I->total_bits;
-        std::vector<unsigned long long> w(W);
+        const double* fo = reinterpret_cast<const double*>(host.data());
+        const unsigned long long* w = reinterpret_cast<const unsigned long long*>(host.data() + 2 * sizeof(double) * k);
         for (int i = 0; i < k; ++i) {
-            CK(cudaMemcpy(w.data(), p->words.as<unsigned long long>() + (size_t)best[i] * W, sizeof(unsigned long long) * W,
-                          cudaMemcpyDeviceToHost));
-            unpack_host_bits(w.data(), nb, bits + (size_t)i * nb);
-            fit[i] = f[best[i]];
-            obj[i] = o[best[i]];
+            unpack_host_bits(w + (size_t)i * I->words, I->total_bits, bits + (size_t)i * I->total_bits);
+            fit[i] = fo[i];
+            obj[i] = fo[k + i];
         }
     });
 }
@@ -1680,44 +1866,26 @@ int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* 
 int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits, const double* fit, const double* obj) {
     return guard([&] {
         if (!c || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
-        if (k < 0 || k > c->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        check_migrants(k, c->n, bits);
         if (k == 0) return;
         ffsga_cuda_instance_t* I = c->inst;
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
-        const int q = c->parity();
-        sort_island_dev(I, c->fit.as<double>() + (size_t)q * c->n, c->n, I->mg_idx_b);
-        std::vector<long long> order(c->n);
-        CK(cudaMemcpyAsync(order.data(), I->mg_idx_b.p, sizeof(long long) * c->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaStreamSynchronize(I->stream));
-        std::vector<long long> storage = cell_storage_index(c);
-        const int W = I->words;
-        std::vector<unsigned long long> words((size_t)W * k), w;
-        std::vector<long long> dst(k);
+        const size_t bytes = packet_bytes(I, 1, k);
+        std::vector<unsigned char> host(bytes);
+        double* fo = reinterpret_cast<double*>(host.data());
+        unsigned long long* w = reinterpret_cast<unsigned long long*>(host.data() + 2 * sizeof(double) * k);
+        std::vector<unsigned long long> one;
         for (int i = 0; i < k; ++i) {
-            pack_host_bits(bits + (size_t)i * I->total_bits, I->total_bits, W, w);
-            std::copy(w.begin(), w.end(), words.begin() + (size_t)i * W);
-            dst[i] = storage[order[c->n - 1 - i]];
+            pack_host_bits(bits + (size_t)i * I->total_bits, I->total_bits, I->words, one);
+            std::copy(one.begin(), one.end(), w + (size_t)i * I->words);
+            fo[i] = fit[i];
+            fo[k + i] = obj[i];
         }
-        DevBuf dw, ddst;
-        upload(dw, words);
-        upload(ddst, dst);
-        CK(launch_unpack_rows(I->d, dw.as<unsigned long long>(), nullptr, c->genes.as<uint8_t>(), (long long)I->block(),
-                              ddst.as<long long>(), k, I->stream));
-        g_launches += 1;
-        std::vector<double> f(c->n), o(c->n);
-        double* df = c->fit.as<double>() + (size_t)q * c->n;
-        double* dob = c->obj.as<double>() + (size_t)q * c->n;
-        CK(cudaMemcpyAsync(f.data(), df, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaMemcpyAsync(o.data(), dob, sizeof(double) * c->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaStreamSynchronize(I->stream));
-        for (int i = 0; i < k; ++i) {
-            f[order[c->n - 1 - i]] = fit[i];
-            o[order[c->n - 1 - i]] = obj[i];
-        }
-        CK(cudaMemcpy(df, f.data(), sizeof(double) * c->n, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dob, o.data(), sizeof(double) * c->n, cudaMemcpyHostToDevice));
-        refresh_stats(c, nullptr, 0);
+        DevBuf pk;
+        pk.alloc(bytes);
+        CK(cudaMemcpyAsync(pk.p, host.data(), bytes, cudaMemcpyHostToDevice, I->stream));
+        import_into_cell(c, k, pk.as<unsigned char>());
         CK(cudaStreamSynchronize(I->stream));
     });
 }
@@ -1725,52 +1893,22 @@ int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits
 int ffsga_cuda_pseudo_import(ffsga_cuda_pseudo p, int k, const int32_t* genes, const double* fit, const double* obj) {
     return guard([&] {
         if (!p || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
-        if (k < 0 || k > p->n) fail(FFSGA_ERR_CONTRACT, "migrate: migrant count exceeds an island population");
+        check_migrants(k, p->n, genes);
         if (k == 0) return;
         ffsga_cuda_instance_t* I = p->inst;
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
-        sort_island_dev(I, p->fit.as<double>(), p->n, I->mg_idx_b);
-        std::vector<long long> order(p->n);
-        CK(cudaMemcpyAsync(order.data(), I->mg_idx_b.p, sizeof(long long) * p->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaStreamSynchronize(I->stream));
         const size_t L = (size_t)I->J * I->S;
-        DevBuf gi, rows, ddst;
+        DevBuf gi, pk;
         gi.alloc(sizeof(int32_t) * L * k);
-        rows.alloc(I->block() * k);
-        CK(cudaMemcpy(gi.p, genes, sizeof(int32_t) * L * k, cudaMemcpyHostToDevice));
-        std::vector<long long> dst(k);
-        for (int i = 0; i < k; ++i) dst[i] = order[p->n - 1 - i];
-        upload(ddst, dst);
-        CK(launch_rows_from_int(I->d, gi.as<int32_t>(), nullptr, rows.as<uint8_t>(), k, I->stream));
-        CK(launch_pack_bits(I->d, rows.as<uint8_t>(), (long long)I->block(), nullptr, p->words.as<unsigned long long>(),
-                            ddst.as<long long>(), k, false, I->dBitStage.as<uint16_t>(), I->stream));
-        g_launches += 2;
-        std::vector<double> f(p->n), o(p->n);
-        CK(cudaMemcpyAsync(f.data(), p->fit.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaMemcpyAsync(o.data(), p->obj.p, sizeof(double) * p->n, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaStreamSynchronize(I->stream));
-        IslandState s = read_state(I, p->st);
-        int take = -1;
-        double af = s.arch_fit;
-        for (int i = 0; i < k; ++i) {
-            f[dst[i]] = fit[i];
-            o[dst[i]] = obj[i];
-            if (fit[i] > af) {  // consider_for_archive in install order (pseudo.cpp:98-113)
-                af = fit[i];
-                take = i;
-            }
-        }
-        CK(cudaMemcpy(p->fit.p, f.data(), sizeof(double) * p->n, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(p->obj.p, o.data(), sizeof(double) * p->n, cudaMemcpyHostToDevice));
-        if (take >= 0) {
-            s.arch_fit = fit[take];
-            s.arch_obj = obj[take];
-            CK(cudaMemcpy(p->st.p, &s, sizeof(s), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(p->archive.p, p->words.as<unsigned long long>() + (size_t)dst[take] * I->words,
-                          sizeof(unsigned long long) * I->words, cudaMemcpyDeviceToDevice));
-        }
-        refresh_stats(nullptr, p, 0);
+        pk.alloc(packet_bytes(I, 0, k));
+        CK(cudaMemcpyAsync(gi.p, genes, sizeof(int32_t) * L * k, cudaMemcpyHostToDevice, I->stream));
+        CK(cudaMemcpyAsync(pk.p, fit, sizeof(double) * k, cudaMemcpyHostToDevice, I->stream));
+        CK(cudaMemcpyAsync(pk.as<double>() + k, obj, sizeof(double) * k, cudaMemcpyHostToDevice, I->stream));
+        CK(launch_rows_from_int(I->d, gi.as<int32_t>(), nullptr, pk.as<uint8_t>() + 2 * sizeof(double) * k, k,
+                                I->stream));
+        g_launches += 1;
+        import_into_pseudo(p, k, pk.as<unsigned char>());
         CK(cudaStreamSynchronize(I->stream));
     });
 }
@@ -1803,6 +1941,16 @@ int ffsga_cuda_timing(ffsga_cuda_instance inst, int which, double* ms, int64_t* 
     });
 }
 
+int ffsga_cuda_timing_busy(ffsga_cuda_instance inst, int which, double* busy_ms) {
+    return guard([&] {
+        if (!inst || which < 0 || which > 2 || !busy_ms) fail(FFSGA_ERR_ARG, "timing_busy: bad argument");
+        std::lock_guard<std::mutex> lk(inst->mu);
+        inst->use();
+        inst->resolve_timing();
+        *busy_ms = inst->t_busy[which];
+    });
+}
+
 int ffsga_cuda_evaluations(ffsga_cuda_instance inst, int64_t* count) {
     return guard([&] {
         if (!inst || !count) fail(FFSGA_ERR_ARG, "null pointer");
@@ -1823,6 +1971,7 @@ int ffsga_cuda_reset_timing(ffsga_cuda_instance inst) {
         inst->resolve_timing();
         for (int i = 0; i < 3; ++i) {
             inst->t_ms[i] = 0;
+            inst->t_busy[i] = 0;
             inst->t_n[i] = 0;
         }
     });

@@ -25,6 +25,7 @@ namespace ffsga_dev {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned long long kNoErr = ~0ull;
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000LL); }
 
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         // One decode of the group's chromosome (stage-0 routing, then every stage).  `work`
         // enters as "decode this group" and leaves false when a gene is out of range; `tie`
         // reports equal consecutive ready times under the ready-only pop order.
-        auto decode = [&](auto exact_tag, bool& work, bool& tie) {
+        auto decode = [&](auto exact_tag, bool& work, bool& tie, unsigned long long& errc) {
             constexpr bool EXACT = decltype(exact_tag)::value;
             if (work) prefetch_row<G>(I, genes, 0, m, row_a);
             tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
@@ -437,8 +438,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             bad_k = group_min_int<G>(bad_k);
             if (work && bad_k != 0x7FFFFFFF) {
                 work = false;
-                if (m == 0 && W.err)
-                    atomicMin(W.err, ((unsigned long long)item << 32) | (unsigned long long)I.rel_order[bad_k]);
+                errc = ((unsigned long long)item << 32) | (unsigned long long)I.rel_order[bad_k];
             }
 
             // ---- stages
@@ -468,9 +468,8 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
                     group_min_key<G>(bc, bj);
                     if (row_bad && work && bj != 0x7FFFFFFF) {
                         work = false;
-                        if (m == 0 && W.err)
-                            atomicMin(W.err, ((unsigned long long)item << 32) |
-                                                 ((unsigned long long)(s + 1) << 16) | (unsigned long long)bj);
+                        errc = ((unsigned long long)item << 32) | ((unsigned long long)(s + 1) << 16) |
+                               (unsigned long long)bj;
                     }
                 }
                 Mprev = Ms;
@@ -479,19 +478,28 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         };
 
         bool work = active, tie = false;
-        decode(std::false_type{}, work, tie);
+        unsigned long long errc = kNoErr;  // first out-of-range gene, reported once the order is exact
+        decode(std::false_type{}, work, tie, errc);
         // Equal ready times met under the ready-only order (integer-valued instances; never seen
         // with continuous processing times): decode those chromosomes again in (ready, job)
-        // order.  CTA-uniform decision, because the stage passes contain CTA barriers.
+        // order.  CTA-uniform decision, because the stage passes contain CTA barriers.  A group
+        // that also met an out-of-range gene after the tie is redone too: which job the reference
+        // names first depends on the exact completions (model.cpp:81-83), so the error of the
+        // exact pass replaces that of the fast one.
         const bool any_tie = I.cta_sync ? (__syncthreads_or(tie) != 0) : __any_sync(kFull, tie);
         if (any_tie) {
             unsigned gt = tie ? 1u : 0u;
 #pragma unroll
             for (int off = G / 2; off > 0; off >>= 1) gt |= __shfl_xor_sync(kFull, gt, off, G);
-            bool redo = gt != 0 && work, tie2 = false;
-            decode(std::true_type{}, redo, tie2);
-            if (gt) work = redo;
+            bool redo = gt != 0 && active, tie2 = false;
+            unsigned long long errc2 = kNoErr;
+            decode(std::true_type{}, redo, tie2, errc2);
+            if (gt) {
+                work = redo;
+                errc = errc2;
+            }
         }
+        if (errc != kNoErr && m == 0 && W.err) atomicMin(W.err, errc);
 
         // ---- report_from_completions (model.cpp:107-120); completions are in lval[0..J)
         double mk = 0.0;
@@ -1416,22 +1424,61 @@ __global__ void k_sort_keys(const double* fit, double* keys, long long n) {
     }
 }
 
-// cellular -> pseudo (migration.cpp:47-57): best[i] of the cellular island lands on
-// worst[N-1-i] of the pseudo island, converted with int_to_bits; the archive absorbs the
-// installs in order (pseudo.cpp:98-104).
-__global__ void k_migrate_c2p(DevInst I, CellIsland C, PseudoIsland P, const long long* best_c,
-                              const long long* worst_p, int k, int parity, const uint16_t* bit_stage) {
+// Migrant packets (cross-device migration, islands.py): k migrants as they leave their island,
+// [fit[k] fp64][obj[k] fp64][payload], payload = k stage-major gene rows of S*Jpad bytes (from a
+// cellular island) or k packed members of W u64 words (from a pseudo island).  An exporter
+// writes one on its own GPU, the bytes travel over NCCL / NVLink, the importer installs them
+// with the same kernels as a device-local migration (migration.cpp:47-69).
+
+// k best cells (sort_island order) -> packet rows + fit/obj
+__global__ void k_export_cell(DevInst I, CellIsland C, const long long* best_c, int k, int parity, uint8_t* rows,
+                              double* fo) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= k) return;
     const long long src = best_c[warp];
+    const size_t block = (size_t)I.S * I.Jpad;
+    const uint4* r = reinterpret_cast<const uint4*>(C.genes + ((size_t)C.sel[(size_t)parity * C.n + src] * C.n + src) * block);
+    uint4* out = reinterpret_cast<uint4*>(rows + (size_t)warp * block);
+    for (size_t v = lane; v < block / 16; v += 32) out[v] = r[v];
+    if (lane == 0) {
+        fo[warp] = C.fit[(size_t)parity * C.n + src];
+        fo[k + warp] = C.obj[(size_t)parity * C.n + src];
+    }
+}
+
+// k best members (sort_island order) -> packet words + fit/obj
+__global__ void k_export_pseudo(DevInst I, PseudoIsland P, const long long* best_p, int k, unsigned long long* words,
+                                double* fo) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= k) return;
+    const long long src = best_p[warp];
+    for (int w = lane; w < I.words; w += 32) words[(size_t)warp * I.words + w] = P.words[src * I.words + w];
+    if (lane == 0) {
+        fo[warp] = P.fit[src];
+        fo[k + warp] = P.obj[src];
+    }
+}
+
+// cellular -> pseudo (migration.cpp:47-57): best[i] of the cellular island (or row i of a packet)
+// lands on worst[N-1-i] of the pseudo island, converted with int_to_bits; the archive absorbs
+// the installs in order (pseudo.cpp:98-104).
+__global__ void k_migrate_c2p(DevInst I, CellIsland C, PseudoIsland P, const long long* best_c,
+                              const long long* worst_p, int k, int parity, const uint16_t* bit_stage,
+                              const uint8_t* pk_rows, const double* pk_fo) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= k) return;
     const long long dst = worst_p[P.n - 1 - warp];
     const size_t block = (size_t)I.S * I.Jpad;
-    const uint8_t* r = C.genes + ((size_t)C.sel[(size_t)parity * C.n + src] * C.n + src) * block;
+    const long long src = pk_rows ? warp : best_c[warp];
+    const uint8_t* r = pk_rows ? pk_rows + (size_t)warp * block
+                               : C.genes + ((size_t)C.sel[(size_t)parity * C.n + src] * C.n + src) * block;
     for (int w = lane; w < I.words; w += 32) P.words[dst * I.words + w] = pack_word(I, r, w, bit_stage);
     if (lane == 0) {
-        P.fit[dst] = C.fit[(size_t)parity * C.n + src];
-        P.obj[dst] = C.obj[(size_t)parity * C.n + src];
+        P.fit[dst] = pk_rows ? pk_fo[warp] : C.fit[(size_t)parity * C.n + src];
+        P.obj[dst] = pk_rows ? pk_fo[k + warp] : C.obj[(size_t)parity * C.n + src];
     }
 }
 
@@ -1455,18 +1502,19 @@ __global__ void k_migrate_archive(DevInst I, PseudoIsland P, const long long* wo
 
 // pseudo -> cellular (migration.cpp:59-69): bits_to_int into the cell's live storage slot.
 __global__ void k_migrate_p2c(DevInst I, PseudoIsland P, CellIsland C, const long long* best_p,
-                              const long long* worst_c, int k, int parity) {
+                              const long long* worst_c, int k, int parity, const unsigned long long* pk_words,
+                              const double* pk_fo) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= k) return;
-    const long long src = best_p[warp];
     const long long dst = worst_c[C.n - 1 - warp];
     const size_t block = (size_t)I.S * I.Jpad;
     uint8_t* r = C.genes + ((size_t)C.sel[(size_t)parity * C.n + dst] * C.n + dst) * block;
-    unpack_member(I, P.words + src * I.words, r, lane);
+    const long long src = pk_words ? warp : best_p[warp];
+    unpack_member(I, (pk_words ? pk_words : P.words) + src * I.words, r, lane);
     if (lane == 0) {
-        C.fit[(size_t)parity * C.n + dst] = P.fit[src];
-        C.obj[(size_t)parity * C.n + dst] = P.obj[src];
+        C.fit[(size_t)parity * C.n + dst] = pk_words ? pk_fo[warp] : P.fit[src];
+        C.obj[(size_t)parity * C.n + dst] = pk_words ? pk_fo[k + warp] : P.obj[src];
     }
 }
 
@@ -1667,17 +1715,34 @@ cudaError_t launch_sort_desc(const double* fit, long long n, double* keys_tmp, d
 
 cudaError_t launch_migrate_c2p(const DevInst& I, const CellIsland& c, const PseudoIsland& p, const long long* best_c,
                                const long long* worst_p, int k, int parity, const uint16_t* bit_stage,
-                               cudaStream_t st) {
+                               cudaStream_t st, const uint8_t* pk_rows, const double* pk_fo) {
     if (k <= 0) return cudaSuccess;
-    k_migrate_c2p<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, c, p, best_c, worst_p, k, parity, bit_stage);
+    k_migrate_c2p<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, c, p, best_c, worst_p, k, parity, bit_stage,
+                                                                       pk_rows, pk_fo);
     k_migrate_archive<<<1, 1024, 0, st>>>(I, p, worst_p, k);
     return cudaGetLastError();
 }
 
 cudaError_t launch_migrate_p2c(const DevInst& I, const PseudoIsland& p, const CellIsland& c, const long long* best_p,
-                               const long long* worst_c, int k, int parity, cudaStream_t st) {
+                               const long long* worst_c, int k, int parity, cudaStream_t st,
+                               const unsigned long long* pk_words, const double* pk_fo) {
     if (k <= 0) return cudaSuccess;
-    k_migrate_p2c<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, p, c, best_p, worst_c, k, parity);
+    k_migrate_p2c<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, p, c, best_p, worst_c, k, parity, pk_words,
+                                                                       pk_fo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_cell(const DevInst& I, const CellIsland& c, const long long* best_c, int k, int parity,
+                               uint8_t* rows, double* fo, cudaStream_t st) {
+    if (k <= 0) return cudaSuccess;
+    k_export_cell<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, c, best_c, k, parity, rows, fo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_pseudo(const DevInst& I, const PseudoIsland& p, const long long* best_p, int k,
+                                 unsigned long long* words, double* fo, cudaStream_t st) {
+    if (k <= 0) return cudaSuccess;
+    k_export_pseudo<<<blocks_for((long long)k * 32, 256), 256, 0, st>>>(I, p, best_p, k, words, fo);
     return cudaGetLastError();
 }
 

@@ -117,12 +117,20 @@ size_t sort_temp_bytes(long long n);
 cudaError_t launch_sort_desc(const double* fit, long long n, double* keys_tmp, double* keys_out,
                              long long* idx_in, long long* idx_out, void* temp, size_t temp_bytes,
                              cudaStream_t st);
+// pk_*: install the k migrants of a packet (rows / words + fit/obj) instead of the source island's
 cudaError_t launch_migrate_c2p(const DevInst& I, const CellIsland& c, const PseudoIsland& p,
                                const long long* best_c, const long long* worst_p, int k, int parity,
-                               const uint16_t* bit_stage, cudaStream_t st);
+                               const uint16_t* bit_stage, cudaStream_t st, const uint8_t* pk_rows = nullptr,
+                               const double* pk_fo = nullptr);
 cudaError_t launch_migrate_p2c(const DevInst& I, const PseudoIsland& p, const CellIsland& c,
                                const long long* best_p, const long long* worst_c, int k, int parity,
-                               cudaStream_t st);
+                               cudaStream_t st, const unsigned long long* pk_words = nullptr,
+                               const double* pk_fo = nullptr);
+// migrant packets: [fit[k]][obj[k]][k rows of S*Jpad bytes | k members of W words]
+cudaError_t launch_export_cell(const DevInst& I, const CellIsland& c, const long long* best_c, int k, int parity,
+                               uint8_t* rows, double* fo, cudaStream_t st);
+cudaError_t launch_export_pseudo(const DevInst& I, const PseudoIsland& p, const long long* best_p, int k,
+                                 unsigned long long* words, double* fo, cudaStream_t st);
 cudaError_t launch_fill_seq(long long* idx, long long n, cudaStream_t st);
 // compute_cell of one cell on an explicit stream state (cellular.cpp:157-162)
 cudaError_t launch_cell_candidate(const DevInst& I, const CellIsland& c, int cell, unsigned long long stream_seed,

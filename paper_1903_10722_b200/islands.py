@@ -108,8 +108,13 @@ class LocalComm:
 
 
 class TorchComm:
-    """torch.distributed plumbing (nccl on GPUs, gloo in the CPU tests).  Only scalar
-    champions (all_gather, 8 B per island) and migrant rows (point-to-point) ever move."""
+    """torch.distributed plumbing.  Only island statistics (all_gather, 32 B per island) and
+    migrant packets (point-to-point, k rows) ever move.
+
+    With NCCL (`device_tensors`) the data plane is device memory end to end: island statistics
+    are copied on the GPU into a tensor that NCCL all-gathers over NVLink, and migrant packets are
+    exported into a CUDA tensor, sent GPU to GPU and installed from it (capi export_packet /
+    import_packet).  With gloo (the CPU tests) the same exchanges go through host arrays."""
 
     def __init__(self, device: Optional[str] = None):
         import torch
@@ -119,6 +124,22 @@ class TorchComm:
         self.world = dist.get_world_size()
         backend = dist.get_backend()
         self.device = device or ("cuda" if backend == "nccl" else "cpu")
+        self.device_tensors = backend == "nccl"
+
+    # device-tensor plane (NCCL)
+    def allgather_tensor(self, t):
+        out = self.torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t.contiguous())
+        return out
+
+    def send_tensor(self, t, dst: int):
+        self.dist.send(t, dst)
+
+    def recv_tensor(self, t, src: int):
+        self.dist.recv(t, src)
+
+    def broadcast_tensor(self, t, src: int):
+        self.dist.broadcast(t, src)
 
     def _t(self, arr):
         return self.torch.from_numpy(np.ascontiguousarray(arr)).to(self.device)
@@ -253,6 +274,11 @@ class IslandModel:
         self.init_seconds = time.perf_counter() - t0
         self.generation = 0
         self.traces = {i: [] for i in self.local}
+        # device-resident exchanges when the comm moves CUDA tensors and the backend exports
+        # device packets (capi); host arrays otherwise (gloo tests, the oracle backend)
+        self.device_plane = bool(getattr(self.comm, "device_tensors", False)) and \
+            hasattr(capi.Cellular, "export_packet")
+        self.device = device
 
     # -- pieces -------------------------------------------------------------------------
     def _cells(self):
@@ -264,6 +290,9 @@ class IslandModel:
     def advance(self, generations: int):
         """Every local island advances `generations` in one joint launch sequence."""
         cells, pseudos = self._cells(), self._pseudos()
+        if not cells and not pseudos:  # a rank that owns no island (world > islands)
+            self.generation += generations
+            return
         tc, tp = self.capi.step(cells, pseudos, generations)
         ci = pi = 0
         for i in sorted(self.local):
@@ -285,14 +314,63 @@ class IslandModel:
         isl = self.local[i]
         return isl.best()[2] if self.cfg.kind(i) == "cellular" else isl.archive()[2]
 
+    def _gather_states(self):
+        """{best fitness, best objective, archive fitness, archive objective} of every island
+        (global order), gathered over the ranks.  Device plane: each island's statistics are
+        copied on its GPU into one tensor that NCCL all-gathers; the host then reads the n x 4
+        values the (host-side, solver.cpp:142-163) policy needs."""
+        n, comm = self.cfg.n_islands, self.comm
+        if self.device_plane:
+            import torch
+            vec = torch.zeros((n, 4), dtype=torch.float64, device=torch.device("cuda", self.device))
+            vec[:, 2] = -1.0
+            for i, isl in self.local.items():
+                isl.state_device(vec[i])
+            allv = comm.allgather_tensor(vec).cpu().numpy()
+        else:
+            vec = np.zeros((n, 4))
+            vec[:, 2] = -1.0
+            for i, isl in self.local.items():
+                _, bf, bo = isl.best()
+                af, ao = (isl.archive()[1], isl.archive()[2]) if self.cfg.kind(i) == "pseudo" else (-1.0, 0.0)
+                vec[i] = (bf, bo, af, ao)
+            allv = comm.allgather(vec.reshape(-1)).reshape(comm.world, n, 4)
+        return np.stack([allv[owner(i, n, comm.world), i] for i in range(n)])
+
+    def _move_migrants(self, src, dst, k, direction):
+        """Rows of a split couple: export on the source's GPU, point-to-point, import on the
+        destination's GPU (migration.cpp:47-69 split at the wire)."""
+        comm, n = self.comm, self.cfg.n_islands
+        osrc, odst = owner(src, n, comm.world), owner(dst, n, comm.world)
+        if self.device_plane:
+            import torch
+            if osrc == comm.rank:
+                comm.send_tensor(self.local[src].export_packet(k), odst)
+            elif odst == comm.rank:
+                kind = 0 if direction == "a_to_b" else 1
+                pk = torch.empty(self.inst.packet_bytes(kind, k), dtype=torch.uint8,
+                                 device=torch.device("cuda", self.device))
+                comm.recv_tensor(pk, osrc)
+                self.local[dst].import_packet(pk, k)
+            return
+        if osrc == comm.rank:
+            rows, f, o = self.local[src].export_best(k)
+            comm.send(np.ascontiguousarray(rows), odst)
+            comm.send(np.stack([f, o]), odst)
+        elif odst == comm.rank:
+            L = self.inst.num_genes
+            width = L if direction == "a_to_b" else self.total_bits
+            dtype = np.int32 if direction == "a_to_b" else np.uint8
+            rows = comm.recv((k, width), dtype, osrc)
+            fo = comm.recv((2, k), np.float64, osrc)
+            self.local[dst].import_worst(rows, fo[0], fo[1])
+
     def rendezvous(self, done: int) -> List[MigrationEvent]:
         """solver.cpp:142-163 for every couple."""
         cfg, comm, n = self.cfg, self.comm, self.cfg.n_islands
-        vec = np.zeros(n)
-        for i in self.local:
-            vec[i] = self._policy_fitness(i)
-        gathered = comm.allgather(vec)
-        fit = np.array([gathered[owner(i, n, comm.world), i] for i in range(n)])
+        st = self._gather_states()
+        fit = np.array([st[i, 2] if (cfg.kind(i) == "pseudo" and cfg.pseudo_fit_from_archive) else st[i, 0]
+                        for i in range(n)])
         events = []
         for c in range(cfg.couples):
             a, b = 2 * c, 2 * c + 1
@@ -306,17 +384,8 @@ class IslandModel:
                     self.capi.migrate_cellular_to_pseudo(self.local[a], self.local[b], k)
                 else:
                     self.capi.migrate_pseudo_to_cellular(self.local[b], self.local[a], k)
-            elif osrc == comm.rank:
-                rows, f, o = self.local[src].export_best(k)
-                comm.send(np.ascontiguousarray(rows), odst)
-                comm.send(np.stack([f, o]), odst)
-            elif odst == comm.rank:
-                L = self.inst.num_genes
-                width = L if direction == "a_to_b" else self.total_bits
-                dtype = np.int32 if direction == "a_to_b" else np.uint8
-                rows = comm.recv((k, width), dtype, osrc)
-                fo = comm.recv((2, k), np.float64, osrc)
-                self.local[dst].import_worst(rows, fo[0], fo[1])
+            elif comm.rank in (osrc, odst):
+                self._move_migrants(src, dst, k, direction)
             events.append(MigrationEvent(done, beta, alpha, direction, k, c))
             # the entries already written for this generation are refreshed (solver.cpp:156-160)
             for i in (a, b):
@@ -346,18 +415,21 @@ class IslandModel:
 
     def finish(self, events, seconds) -> IslandResult:
         cfg, comm, n = self.cfg, self.comm, self.cfg.n_islands
-        G = sum(len(t) for t in next(iter(self.traces.values()))) if self.traces else 0
+        G = self.generation  # every rank advanced the same budget, islands or not
         local_tr = np.zeros((n, G))
-        champ = np.full(n, -np.inf)
         for i in self.local:
             local_tr[i] = np.concatenate(self.traces[i]) if self.traces[i] else np.zeros(0)
-            isl = self.local[i]
-            champ[i] = isl.best()[1] if cfg.kind(i) == "cellular" else isl.archive()[1]
+        st = self._gather_states()
+        # champion fitness: cellular best, pseudo archive (solver.cpp:175-183)
+        champ = np.array([st[i, 0] if cfg.kind(i) == "cellular" else st[i, 2] for i in range(n)])
         if comm.world > 1:
-            tr_all = comm.allgather(local_tr.reshape(-1)).reshape(comm.world, n, G)
-            ch_all = comm.allgather(champ)
+            if self.device_plane:
+                import torch
+                t = torch.from_numpy(local_tr).to(torch.device("cuda", self.device))
+                tr_all = comm.allgather_tensor(t).cpu().numpy()
+            else:
+                tr_all = comm.allgather(local_tr.reshape(-1)).reshape(comm.world, n, G)
             traces = np.stack([tr_all[owner(i, n, comm.world), i] for i in range(n)])
-            champ = np.array([ch_all[owner(i, n, comm.world), i] for i in range(n)])
         else:
             traces = local_tr
         # combined = fold of std::min in island order (solver.cpp:166-173)
@@ -381,8 +453,13 @@ class IslandModel:
             if ob == comm.rank:
                 buf[:L] = chrom
                 buf[L:] = [rep["makespan"], rep["total_tardiness"], rep["objective"], rep["fitness"], rep["emax_used"]]
-            allb = comm.allgather(buf)
-            buf = allb[ob]
+            if self.device_plane:
+                import torch
+                t = torch.from_numpy(buf).to(torch.device("cuda", self.device))
+                comm.broadcast_tensor(t, ob)
+                buf = t.cpu().numpy()
+            else:
+                buf = comm.allgather(buf)[ob]
             chrom = buf[:L].astype(np.int32)
             rep = dict(makespan=buf[L], total_tardiness=buf[L + 1], objective=buf[L + 2], fitness=buf[L + 3],
                        emax_used=buf[L + 4])

@@ -140,6 +140,19 @@ def main():
               "source": f"profiles/{a.tag}_summary.txt (ncu --set full --clock-control none, bench.py GA step)"}
         with open(os.path.join(HERE, f"{a.tag}_traffic.json"), "w") as f:
             json.dump(tr, f, indent=1)
+        # what bench.py reads (roofline.traffic, roofline.issue_roofline): one file per round
+        prof = {"kernel": d["kernel"], "items_in_captured_launch": a.cell_items,
+                "launch_ms": d["gpu__time_duration.sum"],
+                "traffic_bytes_per_eval": (rd + wr) / a.cell_items,
+                "algorithmic_bytes_per_eval": 10016,
+                "achieved_gbs_ncu": 10016 * a.cell_items / (d["gpu__time_duration.sum"] / 1e3) / 1e9,
+                "issue_active": d["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0,
+                "warps_per_sm": d["sm__warps_active.avg.per_cycle_active"],
+                "threads_per_inst": d["smsp__thread_inst_executed_per_inst_executed.ratio"],
+                "smem_bank_conflicts": d.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+                "capture": f"profiles/{a.tag}_summary.txt"}
+        with open(os.path.join(HERE, f"{a.tag}_k1_profile.json"), "w") as f:
+            json.dump(prof, f, indent=1)
     print("\n".join(lines[:20]))
 
 

@@ -44,10 +44,23 @@ def test_bench_two_ranks_functional():
     assert d["config"]["islands_per_rank"] == 4
 
 
-def test_reference_arm_line():
-    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
-                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+def test_reference_arm_line_and_same_trajectory():
+    """Both arms run warm-up + steps generations of the same 8 islands from the same seeds: the
+    per-island best objectives they print are identical (the timed config is the pinned one), and
+    the reference arm loads nothing of the product package."""
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '2']; "
+            "import bench; bench.main(); "
+            "bad = [m for m in sys.modules if m.startswith('paper_1903_10722_b200')]; "
+            "assert not bad, bad")
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    r = last_json(p.stdout)
+    assert r["impl"] == "reference" and r["value"] > 0
+    assert r["e2e"]["h2d_bytes_per_step"] == 0 and r["cpu_baseline"]["kind"] == "reference"
+    assert r["cpu_baseline"]["cpu_model"] and r["cpu_baseline"]["nproc"] >= 1
+    p = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "2", "--no-cpu-baseline",
+                        "--no-sweep"], cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stderr[-3000:]
     d = last_json(p.stdout)
-    assert d["impl"] == "reference" and d["value"] > 0
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "reference"
+    assert d["generations_done"] == r["generations_done"] == 3
+    assert d["island_best_objectives"] == r["island_best_objectives"]

@@ -118,6 +118,40 @@ def test_ready_time_ties_redecoded_exactly(capi, orc, J, S, M):
         assert 0 < ties < 300
 
 
+def test_ties_and_out_of_range_genes_name_the_reference_job(capi, orc):
+    """a chromosome whose earlier stages have equal ready times AND whose later stage
+    holds several out-of-range genes must name the reference's first offender (model.cpp:81-83,
+    minimum (ready, job) in that stage's dispatch order), which depends on the exact tie order."""
+    from pyoracle import InstanceData
+    J, S, M = 30, 5, [3, 2, 3, 2, 3]
+    rng = np.random.default_rng(5)
+    proc = rng.integers(1, 4, size=(J, sum(M))).astype(np.float64)
+    release = rng.integers(0, 3, J).astype(np.float64)
+    d = InstanceData(J, S, M, proc, release, release + 20.0, 1.0)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    pop = oi.random_population(31, 0, 150)
+    checked = 0
+    for i, g in enumerate(pop):
+        g = g.copy()
+        s_bad = 2 + i % 3
+        for j in rng.choice(J, size=6, replace=False):
+            g[j * S + s_bad] = M[s_bad] + int(rng.integers(0, 3))
+        with pytest.raises(ValueError) as a:
+            inst.evaluate([g])
+        with pytest.raises(ValueError) as b:
+            oi.score(g, emax)
+        assert str(a.value).split(" (")[0] == str(b.value), i
+        # the same chromosome inside a batch of good ones (item order, CTA-mixed redo)
+        batch = np.concatenate([pop[:i], g[None, :]])
+        with pytest.raises(ValueError) as c:
+            inst.evaluate(batch)
+        assert str(c.value).split(" (")[0] == str(b.value), i
+        checked += 1
+    assert checked == 150
+
+
 def test_decode_schedule_matches_reference(capi, orc):
     d = synthetic(orc, 50, 6)
     oi = orc.instance(d)

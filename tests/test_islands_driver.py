@@ -108,16 +108,17 @@ def _worker(rank, world, port, couples, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("couples", [1, 2])
-def test_two_ranks_gloo_match_one_process(orc, couples):
+@pytest.mark.parametrize("world,couples", [(2, 1), (2, 2), (3, 1)])
+def test_two_ranks_gloo_match_one_process(orc, world, couples):
     """couples=1: the couple is split over 2 ranks (migrant rows cross ranks);
-    couples=2: one couple per rank (device-local migration)."""
+    couples=2: one couple per rank (device-local migration); world 3 > 2 islands: one rank owns
+    no island and still takes part in every exchange."""
     import multiprocessing as mp
     import oracle_backend as ob
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, couples, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, couples, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]
