@@ -204,6 +204,10 @@ def reference_arm(args):
     if not have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libffsga_ref.so not built"}))
         return 0
+    if args.workload == "c4":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the headline C3 step "
+                          "(default) and the C5 decoder sweep; C4 is a secondary GPU workload"}))
+        return 0
     workers = os.cpu_count() or 1
     ref = RefLib()
     m = synthetic_machines(J, S)
@@ -327,13 +331,84 @@ def decoder_sweep(inst_data, emax, device, steps, warmup):
             "checksum_objective_sum": float(np.sum(obj))}
 
 
+def c4_workload(args, comm, local, world, rank):
+    """C4: 1000 x 20 x [2, 8], 64 islands (32 couples of CellGrid 32x32 +
+    PairPopulation 1024), weight 0, a rendezvous every 10 generations -- so the timed region
+    crosses rendezvous (policy all-gather, decide, migrant packets when k > 0).  Wall clock with
+    the device synchronised on both sides (the rendezvous is host policy + collectives), max over
+    ranks."""
+    import torch
+    from paper_1903_10722_b200 import capi, generate_instance, estimate_emax, instance_arrays
+    from paper_1903_10722_b200.islands import IslandConfig, IslandModel
+    J4, S4, gap = 1000, 20, 10
+    m4 = synthetic_machines(J4, S4)
+    inst = generate_instance(jobs=J4, stages=S4, machines=m4, weight=0.0, seed=GEN_SEED)
+    emax = estimate_emax(inst)
+    cfg = IslandConfig(couples=32, island_population=1024, generations=args.warmup + args.steps, migration_gap=gap,
+                       theta=THETA, seed=RUN_SEED, grid_shape=(32, 32))
+    model = IslandModel(instance_arrays(inst), emax, cfg, comm, device=local)
+
+    def barrier():
+        if comm is not None:
+            comm.barrier()
+
+    def segment(n, done):  # n generations from `done`, rendezvous at the gap boundaries (solver.cpp:128-164)
+        events, t_mig, crossed = [], 0.0, 0
+        end = done + n
+        while done < end:
+            stop = min(end, (done // gap + 1) * gap)
+            model.advance(stop - done)
+            done = stop
+            if done % gap == 0 and done < cfg.generations:
+                tm = time.perf_counter()
+                events += model.rendezvous(done)
+                t_mig += time.perf_counter() - tm
+                crossed += 1
+        return done, events, t_mig, crossed
+
+    done, _, _, _ = segment(args.warmup, 0)
+    torch.cuda.synchronize()
+    barrier()
+    ev0 = model.inst.evaluations()
+    l0 = capi.launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        done, events, t_mig, crossed = segment(args.steps, done)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    barrier()
+    l1 = capi.launch_count()
+    evals = model.inst.evaluations() - ev0
+    if comm is not None:
+        agg = comm.allgather(np.array([dt, t_mig, evals], dtype=np.float64))
+        dt, t_mig, evals_all = float(agg[:, 0].max()), float(agg[:, 1].max()), float(agg[:, 2].sum())
+    else:
+        evals_all = float(evals)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": args.steps / dt, "unit": "generations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (SURVEY 8(d) generator convention, random-init populations)",
+            "config": {"workload": "C4: FFS 1000 jobs x 20 stages x 2-8 machines/stage, 64 islands (32 cellular 32x32 "
+                                   "+ 32 pseudo 1024), weight 0, rendezvous every 10 generations",
+                       "jobs": J4, "stages": S4, "machines": m4, "islands": 64, "population": 65536, "gap": gap,
+                       "weight": 0.0, "ranks": world},
+            "evals_per_s": evals_all / dt, "rendezvous_in_timed_region": crossed,
+            "migrations_in_timed_region": [[e.generation, e.couple, e.direction, e.migrants] for e in events],
+            "rendezvous_s": t_mig,
+            "timing": "wall clock, device synchronised on both sides, max over ranks",
+            "gpu_launches": int(l1 - l0), "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="ga", choices=["ga", "decoder"])
+    ap.add_argument("--workload", default="ga", choices=["ga", "decoder", "c4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
@@ -356,6 +431,13 @@ def main():
         from paper_1903_10722_b200.islands import TorchComm
         comm = TorchComm(device=f"cuda:{local}" if backend == "nccl" else "cpu")
 
+    if args.workload == "c4":
+        rc = c4_workload(args, comm, local, world, rank)
+        if comm is not None:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return rc
     from paper_1903_10722_b200 import capi
     from paper_1903_10722_b200.islands import IslandConfig, IslandModel
     inst, emax = make_instance()

@@ -54,19 +54,25 @@ def _headers(d, exts=(".h", ".cuh", ".hpp")):
     return out
 
 
-def build_cuda(force=False):
-    os.makedirs(BUILD, exist_ok=True)
+def build_cuda(force=False, checked=False):
+    """checked: the same library with device-side bounds and invariant checks (-DFFSGA_CHECKED)
+    into paper_1903_10722_b200/checked/ -- the stand-in for compute-sanitizer."""
+    bdir = os.path.join(BUILD, "checked") if checked else BUILD
+    os.makedirs(bdir, exist_ok=True)
     hdrs = _headers(CSRC) + [os.path.join(ROOT, "include", "ffsga_cuda.h")]
     objs, jobs = [], []
+    extra = ["-DFFSGA_CHECKED"] if checked else []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            jobs.append([NVCC] + ARCH + NVFLAGS + ["-c", s, "-o", o])
+            jobs.append([NVCC] + ARCH + NVFLAGS + extra + ["-c", s, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         list(ex.map(_run, jobs))
-    lib = os.path.join(PKG, "libffsga_cuda.so")
+    if checked:
+        os.makedirs(os.path.join(PKG, "checked"), exist_ok=True)
+    lib = os.path.join(PKG, "checked", "libffsga_cuda.so") if checked else os.path.join(PKG, "libffsga_cuda.so")
     if force or jobs or _newer(lib, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     return lib
@@ -124,8 +130,11 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--skip-oracle", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="also build the checked library (FFSGA_CHECKED)")
     a = ap.parse_args(argv)
     build_cuda(a.force)
+    if a.checked:
+        build_cuda(a.force, checked=True)
     build_host(a.force)
     build_cli(a.force)
     if not a.skip_oracle:

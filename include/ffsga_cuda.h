@@ -226,6 +226,11 @@ int ffsga_cuda_reset_timing(ffsga_cuda_instance inst);
 int ffsga_cuda_evaluations(ffsga_cuda_instance inst, int64_t* count);
 /* device milliseconds of the last ffsga_cuda_step launch sequence (events on its stream) */
 int ffsga_cuda_last_step_ms(ffsga_cuda_instance inst, float* ms);
+/* Diagnostics of a checked build (python build.py --checked -> paper_1903_10722_b200/checked/):
+ * the first device-side bounds / invariant check that failed since the last reset, encoded
+ * code << 48 | a << 24 | b, 0 when none failed; -1 from a normal build.  Synchronises the
+ * device. */
+int ffsga_cuda_checked_status(int reset, int64_t* status);
 /* kernels launched by this library since load (all kinds) */
 int ffsga_cuda_launch_count(int64_t* count);
 

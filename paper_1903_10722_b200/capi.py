@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libffsga_cuda.so")
+# FFSGA_CUDA_LIB: load another build of the same library (the checked build of
+# `python build.py --checked`, paper_1903_10722_b200/checked/libffsga_cuda.so)
+LIB_PATH = os.environ.get("FFSGA_CUDA_LIB") or os.path.join(HERE, "libffsga_cuda.so")
 
 FFSGA_OK, FFSGA_ERR_CONTRACT, FFSGA_ERR_CONFIG, FFSGA_ERR_CUDA, FFSGA_ERR_OOM, FFSGA_ERR_ARG = range(6)
 
@@ -104,6 +106,7 @@ _SIGS = {
     "ffsga_cuda_timing_busy": (_i32, [_vp, _i32, _pd]),
     "ffsga_cuda_reset_timing": (_i32, [_vp]),
     "ffsga_cuda_launch_count": (_i32, [C.POINTER(_i64)]),
+    "ffsga_cuda_checked_status": (_i32, [_i32, C.POINTER(_i64)]),
 }
 
 _lib = None
@@ -143,6 +146,13 @@ def _p(a, t):
 def device_count():
     n = C.c_int(0)
     _check(lib().ffsga_cuda_device_count(C.byref(n)))
+    return n.value
+
+
+def checked_status(reset=True):
+    """First failed device check of a checked build (0 = none), -1 from a normal build."""
+    n = C.c_int64(0)
+    _check(lib().ffsga_cuda_checked_status(int(reset), C.byref(n)))
     return n.value
 
 

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+
+#include <nvtx3/nvToolsExt.h>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -143,6 +145,15 @@ std::string gene_error(unsigned long long code) {
 }
 
 constexpr unsigned long long kNoError = ~0ull;
+
+// NVTX range over one C-ABI call (nsys / ncu --nvtx timelines; header-only NVTX 3, no cost
+// without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace
 
@@ -512,6 +523,7 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
             }
         }
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
+        d.check_selftest = std::getenv("FFSGA_CHECK_SELFTEST") ? 1 : 0;
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("FFSGA_STEP_MIX")) I->step_mix = std::max(0, std::atoi(v));
         mark("devinst");
@@ -562,6 +574,7 @@ int ffsga_cuda_instance_info(ffsga_cuda_instance inst, int* row_stride, int* gro
 int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t n, double* obj, double* fit,
                         double* mk, double* td) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_evaluate");
         if (!inst) fail(FFSGA_ERR_ARG, "null instance");
         std::lock_guard<std::mutex> lk(inst->mu);
         inst->use();
@@ -572,6 +585,7 @@ int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t 
 int ffsga_cuda_evaluate_device(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* obj, double* fit,
                                double* mk, double* td, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_evaluate_device");
         if (!inst) fail(FFSGA_ERR_ARG, "null instance");
         if (n < 0) fail(FFSGA_ERR_CONTRACT, "evaluate: negative batch size");
         if (n == 0) return;
@@ -604,6 +618,7 @@ int ffsga_cuda_evaluate_device(ffsga_cuda_instance inst, const uint8_t* genes, i
 int ffsga_cuda_evaluate_u8(ffsga_cuda_instance inst, const uint8_t* genes, int64_t n, double* obj, double* fit,
                            double* mk, double* td) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_evaluate_u8");
         if (!inst) fail(FFSGA_ERR_ARG, "null instance");
         std::lock_guard<std::mutex> lk(inst->mu);
         inst->use();
@@ -614,6 +629,7 @@ int ffsga_cuda_evaluate_u8(ffsga_cuda_instance inst, const uint8_t* genes, int64
 int ffsga_cuda_decode(ffsga_cuda_instance inst, const int32_t* genes, int32_t* machine, double* start,
                       double* completion, double* report5) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_decode");
         if (!inst || !genes || !machine || !start || !completion) fail(FFSGA_ERR_ARG, "decode: null pointer");
         std::lock_guard<std::mutex> lk(inst->mu);
         inst->use();
@@ -737,6 +753,7 @@ int ffsga_cuda_batch_destroy(ffsga_cuda_batch b) {
 
 int ffsga_cuda_batch_fill_random(ffsga_cuda_batch b, uint64_t base_seed, int64_t first, int64_t n) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_batch_fill_random");
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
         if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_fill_random: n exceeds capacity");
         auto* I = b->inst;
@@ -757,6 +774,7 @@ int ffsga_cuda_batch_upload_u8(ffsga_cuda_batch b, const uint8_t* genes, int64_t
 
 int ffsga_cuda_batch_evaluate(ffsga_cuda_batch b, int64_t n) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_batch_evaluate");
         if (!b) fail(FFSGA_ERR_ARG, "null batch");
         if (n < 0 || n > b->cap) fail(FFSGA_ERR_CONTRACT, "batch_evaluate: n exceeds capacity");
         auto* I = b->inst;
@@ -942,6 +960,7 @@ extern "C" {
 int ffsga_cuda_cellular_create(ffsga_cuda_instance inst, int width, int height, int radius, double xr, double mr,
                                uint64_t seed, const int32_t* init_genes, ffsga_cuda_cellular* out) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_cellular_create");
         if (!inst || !out) fail(FFSGA_ERR_ARG, "cellular_create: null pointer");
         *out = nullptr;
         if (width < 1 || height < 1) fail(FFSGA_ERR_CONFIG, "cellular grid shape does not match cell count");
@@ -1168,6 +1187,7 @@ int ffsga_cuda_cellular_install(ffsga_cuda_cellular c, int index, const int32_t*
 int ffsga_cuda_pseudo_create(ffsga_cuda_instance inst, int population, double xr, uint64_t seed,
                              ffsga_cuda_pseudo* out) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_pseudo_create");
         if (!inst || !out) fail(FFSGA_ERR_ARG, "pseudo_create: null pointer");
         *out = nullptr;
         if (population < 2 || population % 2 != 0)
@@ -1369,6 +1389,7 @@ int ffsga_cuda_pseudo_install(ffsga_cuda_pseudo p, int index, const uint8_t* bit
 int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_pseudo* pseudos, int np,
                     int generations, double* trace_c, double* trace_p) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_step");
         if (nc < 0 || np < 0 || (nc > 0 && !cells) || (np > 0 && !pseudos)) fail(FFSGA_ERR_ARG, "step: bad island list");
         if (generations < 0) fail(FFSGA_ERR_CONTRACT, "step: negative generation count");
         if (nc + np == 0 || generations == 0) return;
@@ -1617,6 +1638,7 @@ extern "C" {
 
 int ffsga_cuda_migrate_cellular_to_pseudo(ffsga_cuda_cellular from, ffsga_cuda_pseudo to, int k) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_migrate_cellular_to_pseudo");
         if (!from || !to) fail(FFSGA_ERR_ARG, "migrate: null island");
         if (from->inst != to->inst) fail(FFSGA_ERR_ARG, "migrate: islands must share one instance");
         check_count(k, from->n, to->n);
@@ -1637,6 +1659,7 @@ int ffsga_cuda_migrate_cellular_to_pseudo(ffsga_cuda_cellular from, ffsga_cuda_p
 
 int ffsga_cuda_migrate_pseudo_to_cellular(ffsga_cuda_pseudo from, ffsga_cuda_cellular to, int k) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_migrate_pseudo_to_cellular");
         if (!from || !to) fail(FFSGA_ERR_ARG, "migrate: null island");
         if (from->inst != to->inst) fail(FFSGA_ERR_ARG, "migrate: islands must share one instance");
         check_count(k, from->n, to->n);
@@ -1740,6 +1763,7 @@ int ffsga_cuda_packet_bytes(ffsga_cuda_instance inst, int from_kind, int k, int6
 
 int ffsga_cuda_cellular_export_device(ffsga_cuda_cellular c, int k, void* packet, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_cellular_export_device");
         if (!c) fail(FFSGA_ERR_ARG, "export: null island");
         check_migrants(k, c->n, packet);
         if (k == 0) return;
@@ -1753,6 +1777,7 @@ int ffsga_cuda_cellular_export_device(ffsga_cuda_cellular c, int k, void* packet
 
 int ffsga_cuda_pseudo_export_device(ffsga_cuda_pseudo p, int k, void* packet, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_pseudo_export_device");
         if (!p) fail(FFSGA_ERR_ARG, "export: null island");
         check_migrants(k, p->n, packet);
         if (k == 0) return;
@@ -1766,6 +1791,7 @@ int ffsga_cuda_pseudo_export_device(ffsga_cuda_pseudo p, int k, void* packet, vo
 
 int ffsga_cuda_cellular_import_device(ffsga_cuda_cellular c, int k, const void* packet, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_cellular_import_device");
         if (!c) fail(FFSGA_ERR_ARG, "import: null island");
         check_migrants(k, c->n, packet);
         if (k == 0) return;
@@ -1779,6 +1805,7 @@ int ffsga_cuda_cellular_import_device(ffsga_cuda_cellular c, int k, const void* 
 
 int ffsga_cuda_pseudo_import_device(ffsga_cuda_pseudo p, int k, const void* packet, void* stream) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_pseudo_import_device");
         if (!p) fail(FFSGA_ERR_ARG, "import: null island");
         check_migrants(k, p->n, packet);
         if (k == 0) return;
@@ -1817,6 +1844,7 @@ int ffsga_cuda_pseudo_state_device(ffsga_cuda_pseudo p, double* out4, void* stre
 // ---- host-buffer export/import: the same packets, staged through host memory
 int ffsga_cuda_cellular_export(ffsga_cuda_cellular c, int k, int32_t* genes, double* fit, double* obj) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_cellular_export");
         if (!c || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
         check_migrants(k, c->n, genes);
         if (k == 0) return;
@@ -1840,6 +1868,7 @@ int ffsga_cuda_cellular_export(ffsga_cuda_cellular c, int k, int32_t* genes, dou
 
 int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* fit, double* obj) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_pseudo_export");
         if (!p || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "export: null pointer");
         check_migrants(k, p->n, bits);
         if (k == 0) return;
@@ -1865,6 +1894,7 @@ int ffsga_cuda_pseudo_export(ffsga_cuda_pseudo p, int k, uint8_t* bits, double* 
 
 int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits, const double* fit, const double* obj) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_cellular_import");
         if (!c || (k > 0 && (!bits || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
         check_migrants(k, c->n, bits);
         if (k == 0) return;
@@ -1892,6 +1922,7 @@ int ffsga_cuda_cellular_import(ffsga_cuda_cellular c, int k, const uint8_t* bits
 
 int ffsga_cuda_pseudo_import(ffsga_cuda_pseudo p, int k, const int32_t* genes, const double* fit, const double* obj) {
     return guard([&] {
+        NvtxRange nvtx_range("ffsga_cuda_pseudo_import");
         if (!p || (k > 0 && (!genes || !fit || !obj))) fail(FFSGA_ERR_ARG, "import: null pointer");
         check_migrants(k, p->n, genes);
         if (k == 0) return;
@@ -1974,6 +2005,16 @@ int ffsga_cuda_reset_timing(ffsga_cuda_instance inst) {
             inst->t_busy[i] = 0;
             inst->t_n[i] = 0;
         }
+    });
+}
+
+int ffsga_cuda_checked_status(int reset, int64_t* status) {
+    return guard([&] {
+        if (!status) fail(FFSGA_ERR_ARG, "null pointer");
+        CK(cudaDeviceSynchronize());
+        long long v = -1;
+        CK(checked_status(&v, reset != 0));
+        *status = (int64_t)v;
     });
 }
 

@@ -9,6 +9,26 @@
 namespace ffsga_dev {
 namespace {
 
+// ---- checked build (python build.py --checked, -DFFSGA_CHECKED): device-side bounds and
+// invariant checks standing in for compute-sanitizer (closed on this GPU pool).  The first
+// failed check is kept as code << 48 | a << 24 | b and read by ffsga_cuda_checked_status();
+// kernels continue (indices stay in range), so a failure never hangs or faults the device.
+#ifdef FFSGA_CHECKED
+__device__ unsigned long long g_check_fail;
+__device__ __forceinline__ void check_fail(unsigned code, unsigned a, unsigned b) {
+    atomicCAS(&g_check_fail, 0ull,
+              ((unsigned long long)code << 48) | ((unsigned long long)(a & 0xFFFFFFu) << 24) | (b & 0xFFFFFFu));
+}
+#define FFSGA_CHECK(cond, code, a, b)                                  \
+    do {                                                               \
+        if (!(cond)) check_fail((code), (unsigned)(a), (unsigned)(b)); \
+    } while (0)
+#else
+#define FFSGA_CHECK(cond, code, a, b) \
+    do {                              \
+    } while (0)
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kNoErr = ~0ull;
 

@@ -23,6 +23,7 @@ struct DevInst {
     int max_warps;  // decoder CTA size cap (0 = smem-limited, at most 16)
     int algo;       // decoder: 0 = k-way merge of per-source lists, 1 = per-stage bucket sort
     int bshift;     // bucket decoder: J << bshift histogram buckets per stage
+    int check_selftest;  // checked build: K1 reports a deliberate failure (proves the channel)
     double weight, emax;
     const int* M;               // [S]
     const int* stage_off;       // [S+1]

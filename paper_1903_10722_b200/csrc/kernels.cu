@@ -62,6 +62,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         const int node = J + 1 + k * G + m;
         hj[k] = live ? (int)link[node] : END;
         hv[k] = live ? lval[node] : dinf();
+        FFSGA_CHECK(hj[k] <= END, 1, hj[k], s);
     }
     heads_sort<NS>(hv, hj);
     uint16_t* mytail = tail + m * G;
@@ -69,6 +70,9 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
 #pragma unroll
         for (int d = 0; d < G; ++d) mytail[d] = (uint16_t)(J + 1 + m * G + d);
     }
+#ifdef FFSGA_CHECKED
+    unsigned long long ck_n = 0, ck_s1 = 0, ck_s2 = 0;
+#endif
     stage_barrier(I.cta_sync);
     if (work && m < Ms) {
         // Software pipelined by two pops: pop i is retired (recurrence, list append, stores) in
@@ -104,6 +108,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             if (!last) {
                 const int d = min(q.g, G - 1);
                 const int t = mytail[d];
+                FFSGA_CHECK(t != END && t < J + 1 + G * G, 4, t, q.j);
                 link[t] = (uint16_t)q.j;
                 lval[t] = c;
                 mytail[d] = (uint16_t)q.j;
@@ -112,14 +117,34 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
         };
         // one pop into slot q (which holds the oldest pending pop, retired first)
+#ifdef FFSGA_CHECKED
+        // invariants of the merge: every pop is a job, its successor a node, the popped ready
+        // times are sorted (strictly in (ready, job) order for the exact comparator), and over
+        // the group's lanes the stage pops every job exactly once (count and two checksums)
+        double ck_v = -dinf();
+        int ck_j = -1;
+#endif
         auto pop = [&](Pend& q, const Pend& prev, int bj) {
             if (!EXACT) eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
+#ifdef FFSGA_CHECKED
+            FFSGA_CHECK(bj >= 0 && bj < J, 2, bj, s);
+            if (EXACT)
+                FFSGA_CHECK(key_lt(ck_v, ck_j, hv[0], bj), 6, bj, s);
+            else
+                FFSGA_CHECK(!(hv[0] < ck_v), 5, bj, s);
+            ck_v = hv[0];
+            ck_j = bj;
+            ck_n += 1;
+            ck_s1 += (unsigned long long)bj;
+            ck_s2 += (unsigned long long)bj * (unsigned long long)bj;
+#endif
             int nh;
             double nr;
             if (EARLY) {
                 nh = link[bj];
                 nr = lval[bj];
             }
+            FFSGA_CHECK(!EARLY || nh <= END, 3, nh, bj);
             if (q.j != END) retire(q);
             q.br = hv[0];
             q.p = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32
@@ -196,6 +221,20 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
         }
     }
+#ifdef FFSGA_CHECKED
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        ck_n += __shfl_xor_sync(kFull, ck_n, off, G);
+        ck_s1 += __shfl_xor_sync(kFull, ck_s1, off, G);
+        ck_s2 += __shfl_xor_sync(kFull, ck_s2, off, G);
+    }
+    if (work && m == 0) {
+        const unsigned long long Ju = (unsigned long long)J;
+        FFSGA_CHECK(ck_n == Ju, 7, ck_n, s);
+        FFSGA_CHECK(ck_s1 == Ju * (Ju - 1) / 2, 8, ck_s1, s);
+        FFSGA_CHECK(ck_s2 == (Ju - 1) * Ju * (2 * Ju - 1) / 6, 9, ck_s2, s);
+    }
+#endif
     stage_barrier(I.cta_sync);
 }
 
@@ -263,6 +302,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
     const int J = I.J, S = I.S;
     const int END = J;
     const long long n = W.n_dev ? *W.n_dev + W.n : W.n;  // fused GA list: n cells + device count
+    FFSGA_CHECK(!I.check_selftest, 99, blockIdx.x, threadIdx.x);
 
     // All groups of the CTA share the item loop (CTA-uniform bounds: stage barriers).  A launch
     // that owns the GPU deals items round-robin over the CTAs (group g of CTA b takes item
@@ -317,6 +357,7 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             }
             if (work) {
                 const int t = tail[m];
+                FFSGA_CHECK(t != END && t < J + 1 + G * G, 10, t, m);
                 link[t] = (uint16_t)END;
                 lval[t] = dinf();
             }
@@ -929,6 +970,8 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
     }
 
     const size_t block = (size_t)I.S * I.Jpad;
+    FFSGA_CHECK(p1 >= 0 && p1 < n && p2 >= 0 && p2 < n, 20, p1, p2);
+    FFSGA_CHECK(selq[p1] <= 1 && selq[p2] <= 1 && lo <= hi && hi <= L, 21, lo, hi);
     const uint8_t* g1 = C.genes + ((size_t)selq[p1] * n + p1) * block;
     const uint8_t* g2 = C.genes + ((size_t)selq[p2] * n + p2) * block;
 
@@ -1062,6 +1105,7 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
                 j -= (j * I.S > gene) ? 1 : 0;
                 j += ((j + 1) * I.S <= gene) ? 1 : 0;
                 const int s = gene - j * I.S;
+                FFSGA_CHECK(j >= 0 && j < I.J && s >= 0 && s < I.S, 22, gene, cell);
                 child[(size_t)s * I.Jpad + j] = (uint8_t)index_of(draw(cs, p0 + t), __ldg(I.M + s));
             }
         }
@@ -1625,6 +1669,25 @@ cudaError_t launch_cell_candidate(const DevInst& I, const CellIsland& c, int cel
                                   int parity, uint8_t* out, unsigned long long* draws, cudaStream_t st) {
     k_cell_candidate<<<1, 32, 0, st>>>(I, c, cell, stream_seed, parity, out, draws);
     return cudaGetLastError();
+}
+
+// checked build: the first failed device check (0 = none) and reset; -1 in a normal build
+cudaError_t checked_status(long long* status, bool reset) {
+#ifdef FFSGA_CHECKED
+    unsigned long long v = 0;
+    cudaError_t e = cudaMemcpyFromSymbol(&v, g_check_fail, sizeof(v));
+    if (e != cudaSuccess) return e;
+    *status = (long long)v;
+    if (reset) {
+        v = 0;
+        return cudaMemcpyToSymbol(g_check_fail, &v, sizeof(v));
+    }
+    return cudaSuccess;
+#else
+    (void)reset;
+    *status = -1;
+    return cudaSuccess;
+#endif
 }
 
 cudaError_t launch_fill_seq(long long* idx, long long n, cudaStream_t st) {

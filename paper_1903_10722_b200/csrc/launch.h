@@ -132,6 +132,8 @@ cudaError_t launch_export_cell(const DevInst& I, const CellIsland& c, const long
 cudaError_t launch_export_pseudo(const DevInst& I, const PseudoIsland& p, const long long* best_p, int k,
                                  unsigned long long* words, double* fo, cudaStream_t st);
 cudaError_t launch_fill_seq(long long* idx, long long n, cudaStream_t st);
+// checked build (-DFFSGA_CHECKED): first failed device check, 0 = none; -1 in a normal build
+cudaError_t checked_status(long long* status, bool reset);
 // compute_cell of one cell on an explicit stream state (cellular.cpp:157-162)
 cudaError_t launch_cell_candidate(const DevInst& I, const CellIsland& c, int cell, unsigned long long stream_seed,
                                   int parity, uint8_t* out, unsigned long long* draws, cudaStream_t st);

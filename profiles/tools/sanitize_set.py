@@ -1,5 +1,9 @@
-"""Reduced parity set for compute-sanitizer (racecheck / memcheck / synccheck / initcheck).
+"""Reduced parity set for the checked build (device-side bounds and invariant checks standing in
+for compute-sanitizer, which this GPU pool does not allow), or for compute-sanitizer itself where
+it is available.
 
+    python build.py --checked
+    FFSGA_CUDA_LIB=paper_1903_10722_b200/checked/libffsga_cuda.so python profiles/tools/sanitize_set.py
     compute-sanitizer --tool racecheck python profiles/tools/sanitize_set.py [--algo bucket]
 
 Exercises every kernel of the library at sizes the sanitizers finish in minutes, and checks
@@ -119,7 +123,15 @@ def main():
     a2.import_packet(b2.export_packet(5), 5)
     assert np.array_equal(a1.genes(), a2.genes()) and np.array_equal(b1.members(), b2.members())
     checks += 1
-    print(f"sanitize_set ({a.algo}): {checks} groups of checks equal to the oracle")
+    st = capi.checked_status(reset=True)
+    assert st in (0, -1), f"device check {st >> 48} failed (a={(st >> 24) & 0xFFFFFF}, b={st & 0xFFFFFF})"
+    if st == 0:  # the failure channel itself: an instance created with FFSGA_CHECK_SELFTEST
+        os.environ["FFSGA_CHECK_SELFTEST"] = "1"
+        capi.Instance.from_data(micro, 211.0).evaluate([[0, 0, 0, 0]])
+        del os.environ["FFSGA_CHECK_SELFTEST"]
+        assert capi.checked_status(reset=True) >> 48 == 99, "a deliberate device check failure was not reported"
+    print(f"sanitize_set ({a.algo}): {checks} groups of checks equal to the oracle; "
+          f"device checks: {'not a checked build' if st == -1 else 'all passed'}")
 
 
 if __name__ == "__main__":

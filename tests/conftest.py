@@ -34,3 +34,14 @@ def synthetic(orc, jobs, stages, lo=2, hi=8, weight=100.0, seed=7, integer_times
     from pyoracle import synthetic_machines
     m = synthetic_machines(jobs, stages, lo, hi)
     return orc.generate(jobs, stages, m, weight=weight, seed=seed, integer_times=integer_times)
+
+
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    """With FFSGA_CUDA_LIB pointing at the checked build (python build.py --checked), every GPU
+    test also asserts that no device-side bounds / invariant check failed during it."""
+    yield
+    if os.environ.get("FFSGA_CUDA_LIB") and request.node.get_closest_marker("gpu"):
+        from paper_1903_10722_b200 import capi
+        st = capi.checked_status(reset=True)
+        assert st == 0, f"device check {st >> 48} failed (a={(st >> 24) & 0xFFFFFF}, b={st & 0xFFFFFF})"
