@@ -43,5 +43,5 @@ def _device_checks(request):
     yield
     if os.environ.get("FFSGA_CUDA_LIB") and request.node.get_closest_marker("gpu"):
         from paper_1903_10722_b200 import capi
-        st = capi.checked_status(reset=True)
-        assert st == 0, f"device check {st >> 48} failed (a={(st >> 24) & 0xFFFFFF}, b={st & 0xFFFFFF})"
+        st = capi.checked_status(reset=True)  # -1: the library is not a checked build
+        assert st in (0, -1), f"device check {st >> 48} failed (a={(st >> 24) & 0xFFFFFF}, b={st & 0xFFFFFF})"
