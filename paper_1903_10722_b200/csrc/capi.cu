@@ -1400,6 +1400,14 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
             if (!pseudos[i] || pseudos[i]->inst != I) fail(FFSGA_ERR_ARG, "step: islands must share one instance");
         std::lock_guard<std::mutex> lk(I->mu);
         I->use();
+        const bool dbg = std::getenv("FFSGA_DEBUG_STEP") != nullptr;  // host-side phase timing
+        auto t_last = std::chrono::steady_clock::now();
+        auto mark = [&](const char* what) {
+            if (!dbg) return;
+            const auto t = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "step %-24s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+            t_last = t;
+        };
         // Descriptors of this joint step.  The islands are split into step groups (up to
         // step_split contiguous groups of each kind) and every group runs its own breed ->
         // evaluate -> commit chain on its own stream: groups never read each other between
@@ -1557,6 +1565,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         // graphs pay off when a generation is launch bound (small islands); capturing costs
         // ~0.1 s, so large work lists run plain launches
         const bool use_graph = !I->timing && generations >= 2 && cap <= 16384 && !std::getenv("FFSGA_NO_GRAPH");
+        mark("setup");
         CK(cudaEventRecord(I->st0, I->stream));
         if (use_graph) {
             // the generation sequence is launch-bound for small islands: capture a chunk of
@@ -1594,6 +1603,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
         }
         g_launches += per_gen * generations;
         CK(cudaEventRecord(I->st1, I->stream));
+        mark("enqueue");
         I->step_recorded = true;
         for (int i = 0; i < nc; ++i) {
             if (trace_c)
@@ -1606,6 +1616,7 @@ int ffsga_cuda_step(const ffsga_cuda_cellular* cells, int nc, const ffsga_cuda_p
                                    cudaMemcpyDeviceToHost, I->stream));
         }
         CK(cudaStreamSynchronize(I->stream));
+        mark("traces+sync");
         for (int i = 0; i < nc; ++i) cells[i]->gen += (unsigned long long)generations;
         for (int i = 0; i < np; ++i) pseudos[i]->gen += (unsigned long long)generations;
     });
