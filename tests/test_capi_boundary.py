@@ -51,3 +51,20 @@ def test_product_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
                 src = open(os.path.join(base, fn), errors="ignore").read()
                 assert "pyoracle" not in src and "ffsga_oracle" not in src and "liboracle" not in src, fn
+
+
+def test_device_plane_entry_points_validate_arguments():
+    """The device-packet entry points reject bad arguments before touching the device (runs
+    without a GPU): the same status codes as the rest of the C ABI."""
+    from paper_1903_10722_b200 import capi
+    L = capi.lib()
+    n = ctypes.c_int64(0)
+    assert L.ffsga_cuda_packet_bytes(None, 0, 1, ctypes.byref(n)) == capi.FFSGA_ERR_ARG
+    for f in (L.ffsga_cuda_cellular_export_device, L.ffsga_cuda_pseudo_export_device,
+              L.ffsga_cuda_cellular_import_device, L.ffsga_cuda_pseudo_import_device):
+        assert f(None, 1, None, None) == capi.FFSGA_ERR_ARG
+        assert "null island" in L.ffsga_cuda_last_error().decode()
+    for f in (L.ffsga_cuda_cellular_state_device, L.ffsga_cuda_pseudo_state_device):
+        assert f(None, None, None) == capi.FFSGA_ERR_ARG
+    assert L.ffsga_cuda_timing_busy(None, 0, None) == capi.FFSGA_ERR_ARG
+    assert L.ffsga_cuda_checked_status(0, None) == capi.FFSGA_ERR_ARG

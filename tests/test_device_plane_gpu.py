@@ -198,3 +198,18 @@ def test_island_driver_over_nccl_two_gpus(tmp_path):
     want = isl.IslandModel(as_data(inst), ffsga.estimate_emax(inst), cfg).run()
     assert got["comb"] == list(want.trace_combined) and got["chrom"] == list(want.best_chromosome)
     assert got["mig"] == len(want.migrations) > 0
+
+
+def test_packet_argument_errors():
+    import torch
+    inst = ffsga.generate_instance(jobs=6, stages=2, machines=[2, 2], seed=3)
+    ci = capi.Instance.from_data(as_data(inst), ffsga.estimate_emax(inst))
+    c, p = capi.Cellular(ci, 4, 4, 1), capi.Pseudo(ci, 8, 2)
+    with pytest.raises(ValueError, match="exceeds an island population"):
+        c.export_packet(17)
+    with pytest.raises(ValueError, match="exceeds an island population"):
+        p.import_packet(torch.zeros(ci.packet_bytes(0, 9), dtype=torch.uint8, device="cuda"), 9)
+    with pytest.raises(ValueError):
+        c.export_packet(3, out=torch.zeros(4, dtype=torch.uint8, device="cuda"))  # too small
+    assert ci.packet_bytes(0, 0) == 0 and c.export_packet(0).numel() == 1  # k = 0: nothing moves
+    assert ci.packet_bytes(1, 3) == 3 * (16 + 8 * ((ci.info()["total_bits"] + 63) // 64))
