@@ -54,6 +54,12 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     const int END = J;
     constexpr bool last = LAST;
     const double* pcol = I.procT + (size_t)(I.stage_off[s] + (m < Ms ? m : 0)) * (J + 1);
+    // The column pointer and the gene row's shared-window address are pinned in registers:
+    // left to itself the compiler refolds them into the pop loop (a 64-bit index add + shift +
+    // constant-bank reload of procT per pop, and S2R SR_CgaCtaId + LEA per pop for the row).
+    asm volatile("" : "+l"(pcol));
+    unsigned row_s = (unsigned)__cvta_generic_to_shared(row);
+    asm volatile("" : "+r"(row_s));
     double hv[NS];
     int hj[NS];
 #pragma unroll
@@ -148,7 +154,13 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             if (q.j != END) retire(q);
             q.br = hv[0];
             q.p = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32
-            q.g = last ? 0 : (int)row[bj];
+            if (last) {
+                q.g = 0;
+            } else {
+                unsigned g;
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(g) : "r"(row_s + (unsigned)bj));
+                q.g = (int)g;
+            }
             q.j = bj;
             if (!EARLY) {
                 nh = link[bj];
@@ -156,8 +168,13 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
             heads_replace_min<NS, EXACT>(hv, hj, nr, nh);
         };
-        if constexpr (DEPTH == 2) {
+        if constexpr (DEPTH == 2 || DEPTH == 4) {
             bool a_older = true;  // which pending slot holds the older pop at loop exit
+            if constexpr (DEPTH == 4) {
+            // "DEPTH 4": the two-slot pipeline unrolled four pops deep (J >= 256): the register
+            // copies the compiler inserts at the loop's back edge are paid once per four pops,
+            // and the longer body schedules better (500x20 +2.4 %; at 100x10 the larger body
+            // costs 11 %, so small instances keep the two-pop body)
             while (true) {
                 int bj = hj[0];
                 if (bj == END) break;
@@ -168,6 +185,28 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                     break;
                 }
                 pop(B, A, bj);
+                bj = hj[0];
+                if (bj == END) break;
+                pop(A, B, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    a_older = false;
+                    break;
+                }
+                pop(B, A, bj);
+            }
+            } else {
+            while (true) {
+                int bj = hj[0];
+                if (bj == END) break;
+                pop(A, B, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    a_older = false;
+                    break;
+                }
+                pop(B, A, bj);
+            }
             }
             tie |= eq;
             if (a_older) {
@@ -1469,6 +1508,9 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
         if (I.algo != 1 && I.J >= 1000) {
             cfg->depth = 3;
             k0 = (const void*)k_eval<8, false, 3>;
+        } else if (I.algo != 1 && I.J >= 256) {
+            cfg->depth = 4;
+            k0 = (const void*)k_eval<8, false, 4>;
         }
     }
     const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true, 2>;
@@ -1520,6 +1562,10 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
         if constexpr (G == 8) {
             if (cfg.depth == 3) {
                 k_eval<8, false, 3><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                return cudaGetLastError();
+            }
+            if (cfg.depth == 4) {
+                k_eval<8, false, 4><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
                 return cudaGetLastError();
             }
         }
