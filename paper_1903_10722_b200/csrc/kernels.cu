@@ -219,8 +219,23 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         } else {  // three pops in flight (large J: the procT slice misses L1 more often)
             Pend C{qnan, 0.0, 0, END};
             int exit_at = 0;  // the slot the loop stopped before holds the oldest pending pop
-            while (true) {
+            while (true) {  // unrolled six pops deep (see DEPTH 4)
                 int bj = hj[0];
+                if (bj == END) break;
+                pop(A, C, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    exit_at = 1;
+                    break;
+                }
+                pop(B, A, bj);
+                bj = hj[0];
+                if (bj == END) {
+                    exit_at = 2;
+                    break;
+                }
+                pop(C, B, bj);
+                bj = hj[0];
                 if (bj == END) break;
                 pop(A, C, bj);
                 bj = hj[0];
@@ -1505,10 +1520,12 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
     cfg->depth = 2;
     const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false, 2>;
     if constexpr (G == 8) {
-        if (I.algo != 1 && I.J >= 1000) {
+        const char* dv = getenv("FFSGA_EVAL_DEPTH");  // experiments: 2, 3 or 4
+        const int want = dv ? atoi(dv) : (I.J >= 1000 ? 3 : (I.J >= 256 ? 4 : 2));
+        if (I.algo != 1 && want == 3) {
             cfg->depth = 3;
             k0 = (const void*)k_eval<8, false, 3>;
-        } else if (I.algo != 1 && I.J >= 256) {
+        } else if (I.algo != 1 && want == 4) {
             cfg->depth = 4;
             k0 = (const void*)k_eval<8, false, 4>;
         }
