@@ -171,7 +171,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         if constexpr (DEPTH == 2 || DEPTH == 4) {
             bool a_older = true;  // which pending slot holds the older pop at loop exit
             if constexpr (DEPTH == 4) {
-            // "DEPTH 4": the two-slot pipeline unrolled four pops deep (J >= 256): the register
+            // "DEPTH 4": the two-slot pipeline unrolled four pops deep (J >= 300): the register
             // copies the compiler inserts at the loop's back edge are paid once per four pops,
             // and the longer body schedules better (500x20 +2.4 %; at 100x10 the larger body
             // costs 11 %, so small instances keep the two-pop body)
@@ -1521,7 +1521,9 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
     const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false, 2>;
     if constexpr (G == 8) {
         const char* dv = getenv("FFSGA_EVAL_DEPTH");  // experiments: 2, 3 or 4
-        const int want = dv ? atoi(dv) : (I.J >= 1000 ? 3 : (I.J >= 256 ? 4 : 2));
+        // measured thresholds (C5 shapes, M in [2, 8]): the 4-deep body wins from J = 300 on
+        // (256x10: 44.4 vs 32.0 M evals/s for the 2-deep body; 300x10 and 256x20: equal)
+        const int want = dv ? atoi(dv) : (I.J >= 1000 ? 3 : (I.J >= 300 ? 4 : 2));
         if (I.algo != 1 && want == 3) {
             cfg->depth = 3;
             k0 = (const void*)k_eval<8, false, 3>;

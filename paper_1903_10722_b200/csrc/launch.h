@@ -78,7 +78,7 @@ struct WorkList {
 struct EvalConfig {
     int G, warps, groups_per_cta, blocks_per_sm;
     int depth;   // K1 pipeline: 2 = two pops in flight, body unrolled 2x; 4 = two in flight, unrolled
-                 // 4x (J >= 256); 3 = three in flight (J >= 1000)
+                 // 4x (J >= 300); 3 = three in flight, unrolled 6x (J >= 1000)
     GroupLayout gl;
     BucketLayout bl;
     size_t smem;
