@@ -604,10 +604,13 @@ def main():
         host = b.download(0, 4096).astype(np.uint8)
         n_e2e = 65536
         hostbig = np.ascontiguousarray(np.tile(host, (n_e2e // 4096, 1)))
-        t0 = time.perf_counter()
-        for _ in range(2):
+        ci.evaluate(hostbig)  # untimed: the first call allocates the pinned staging pair
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
             ci.evaluate(hostbig)
-        e2e = 2 * n_e2e / (time.perf_counter() - t0)
+            ts.append(time.perf_counter() - t0)
+        e2e = n_e2e / float(np.median(ts))
         if rank == 0:
             achieved = SWEEP_N * (L + 16) / (tot / args.steps / 1e3) / 1e9
             print(json.dumps({

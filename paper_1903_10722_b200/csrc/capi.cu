@@ -12,6 +12,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include <nvtx3/nvToolsExt.h>
 #include <numeric>
@@ -185,6 +186,13 @@ struct ffsga_cuda_instance_t {
     // evaluate() staging
     DevBuf ev_in, ev_rows, ev_obj, ev_fit, ev_mk, ev_td, ev_err;
     long long ev_cap = 0;
+    // host-batch evaluation pipeline (evaluate_host): pinned staging pair, copy stream, second
+    // device input buffer, whole-batch results and per-sub-batch error slots
+    void* pin[2] = {nullptr, nullptr};
+    size_t pin_bytes = 0;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t pin_free[2] = {nullptr, nullptr}, in_ready[2] = {nullptr, nullptr}, in_free[2] = {nullptr, nullptr};
+    DevBuf ev_in2, ev_res, ev_errs;
     // migration scratch
     DevBuf mg_keys0, mg_keys1, mg_idx0, mg_idx_a, mg_idx_b, mg_temp;
     // timing: event pairs recorded around launches, resolved lazily (no sync in the timed path)
@@ -206,6 +214,13 @@ struct ffsga_cuda_instance_t {
     void use() const { CK(cudaSetDevice(device)); }
     ~ffsga_cuda_instance_t() {
         cudaSetDevice(device);
+        if (cstream) cudaStreamSynchronize(cstream);
+        for (int k = 0; k < 2; ++k) {
+            if (pin[k]) cudaFreeHost(pin[k]);
+            for (cudaEvent_t e : {pin_free[k], in_ready[k], in_free[k]})
+                if (e) cudaEventDestroy(e);
+        }
+        if (cstream) cudaStreamDestroy(cstream);
         if (stream) cudaStreamDestroy(stream);
         for (auto s : side) cudaStreamDestroy(s);
         for (auto e : side_join) cudaEventDestroy(e);
@@ -292,10 +307,10 @@ namespace {
 
 // Evaluate n device rows into device outputs; returns the first gene error code or kNoError.
 void eval_rows(ffsga_cuda_instance_t* I, const uint8_t* rows, long long n, double* obj, double* fit, double* mk,
-               double* td, bool check) {
+               double* td, bool check, unsigned long long* err = nullptr) {
     if (n <= 0) return;
     I->ev_err.ensure(sizeof(unsigned long long));
-    if (check) CK(cudaMemsetAsync(I->ev_err.p, 0xFF, sizeof(unsigned long long), I->stream));
+    if (check && !err) CK(cudaMemsetAsync(I->ev_err.p, 0xFF, sizeof(unsigned long long), I->stream));
     EvalItems W{};
     W.n = n;
     W.base = rows;
@@ -305,7 +320,7 @@ void eval_rows(ffsga_cuda_instance_t* I, const uint8_t* rows, long long n, doubl
     W.fit = fit;
     W.mk = mk;
     W.td = td;
-    W.err = I->ev_err.as<unsigned long long>();
+    W.err = err ? err : I->ev_err.as<unsigned long long>();
     I->timed(0, [&] { CK(launch_eval(I->d, I->ec, W, n, I->sm_count, false, I->stream)); });
     g_launches += 1;
 }
@@ -329,6 +344,28 @@ void ensure_eval_staging(ffsga_cuda_instance_t* I, long long chunk) {
     I->ev_cap = chunk;
 }
 
+// Host-to-pinned copy of one sub-batch, split over a few threads for large ones (a single
+// memcpy thread moves ~10 GB/s, below PCIe).
+void staged_copy(void* dst, const void* src, size_t bytes) {
+    const size_t per = (size_t)8 << 20;
+    const int nt = (int)std::min<size_t>(8, (bytes + per - 1) / per);
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t part = (bytes + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        const size_t o = (size_t)t * part;
+        if (o >= bytes) break;
+        th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(part, bytes - o)); });
+    }
+    for (auto& x : th) x.join();
+}
+
+// Evaluator::score over a host batch, pipelined in sub-batches: the host copies sub-batch k+1
+// into pinned staging while the copy stream moves sub-batch k to the device and the instance
+// stream transposes and decodes the one before; results stay on the device until one copy back.
 template <typename T>
 void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* obj, double* fit, double* mk,
                    double* td) {
@@ -336,25 +373,66 @@ void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* 
     if (n == 0) return;
     if (!genes || !obj || !fit) fail(FFSGA_ERR_ARG, "evaluate: null pointer");
     const long long L = (long long)I->J * I->S;
-    const long long chunk = std::min<long long>(n, 1 << 16);
-    ensure_eval_staging(I, chunk);
-    for (long long first = 0; first < n; first += chunk) {
-        const long long c = std::min<long long>(chunk, n - first);
-        CK(cudaMemcpyAsync(I->ev_in.p, genes + first * L, sizeof(T) * c * L, cudaMemcpyHostToDevice, I->stream));
-        if (sizeof(T) == 4)
-            CK(launch_rows_from_int(I->d, I->ev_in.as<int32_t>(), nullptr, I->ev_rows.as<uint8_t>(), c, I->stream));
-        else
-            CK(launch_rows_from_int(I->d, nullptr, I->ev_in.as<uint8_t>(), I->ev_rows.as<uint8_t>(), c, I->stream));
-        g_launches += 1;
-        eval_rows(I, I->ev_rows.as<uint8_t>(), c, I->ev_obj.as<double>(), I->ev_fit.as<double>(),
-                  I->ev_mk.as<double>(), I->ev_td.as<double>(), true);
-        CK(cudaMemcpyAsync(obj + first, I->ev_obj.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
-        CK(cudaMemcpyAsync(fit + first, I->ev_fit.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
-        if (mk) CK(cudaMemcpyAsync(mk + first, I->ev_mk.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
-        if (td) CK(cudaMemcpyAsync(td + first, I->ev_td.p, sizeof(double) * c, cudaMemcpyDeviceToHost, I->stream));
-        const unsigned long long code = read_error(I);
-        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
+    // sub-batches of >= 8192 chromosomes keep every decoder round full; at most ~64 MB staged
+    const long long sub = std::min<long long>(n, std::max<long long>(8192, (64ll << 20) / (L * (long long)sizeof(T))));
+    const long long nsub = (n + sub - 1) / sub;
+    const size_t in_bytes = (size_t)sub * L * sizeof(T);
+    ensure_eval_staging(I, sub);
+    I->ev_in2.ensure(in_bytes);
+    I->ev_res.ensure(sizeof(double) * 4 * (size_t)n);
+    I->ev_errs.ensure(sizeof(unsigned long long) * (size_t)nsub);
+    if (!I->cstream) {
+        CK(cudaStreamCreateWithFlags(&I->cstream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k)
+            for (cudaEvent_t* e : {&I->pin_free[k], &I->in_ready[k], &I->in_free[k]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    if (I->pin_bytes < in_bytes) {
+        for (int k = 0; k < 2; ++k) {
+            if (I->pin[k]) CK(cudaFreeHost(I->pin[k]));
+            I->pin[k] = nullptr;
+        }
+        I->pin_bytes = 0;
+        for (int k = 0; k < 2; ++k) CK(cudaHostAlloc(&I->pin[k], in_bytes, cudaHostAllocDefault));
+        I->pin_bytes = in_bytes;
+    }
+    double* robj = I->ev_res.as<double>();
+    double* rfit = robj + n;
+    double* rmk = rfit + n;
+    double* rtd = rmk + n;
+    unsigned long long* errs = I->ev_errs.as<unsigned long long>();
+    CK(cudaMemsetAsync(errs, 0xFF, sizeof(unsigned long long) * (size_t)nsub, I->stream));
+    uint8_t* din[2] = {I->ev_in.as<uint8_t>(), I->ev_in2.as<uint8_t>()};
+    for (long long k = 0; k < nsub; ++k) {
+        const int b = (int)(k & 1);
+        const long long first = k * sub, c = std::min<long long>(sub, n - first);
+        const size_t bytes = (size_t)c * L * sizeof(T);
+        if (k >= 2) CK(cudaEventSynchronize(I->pin_free[b]));  // sub-batch k-2 has left staging
+        staged_copy(I->pin[b], genes + first * L, bytes);
+        if (k >= 2) CK(cudaStreamWaitEvent(I->cstream, I->in_free[b], 0));  // ... and its device input
+        CK(cudaMemcpyAsync(din[b], I->pin[b], bytes, cudaMemcpyHostToDevice, I->cstream));
+        CK(cudaEventRecord(I->pin_free[b], I->cstream));
+        CK(cudaEventRecord(I->in_ready[b], I->cstream));
+        CK(cudaStreamWaitEvent(I->stream, I->in_ready[b], 0));
+        if (sizeof(T) == 4)
+            CK(launch_rows_from_int(I->d, reinterpret_cast<const int32_t*>(din[b]), nullptr, I->ev_rows.as<uint8_t>(), c,
+                                    I->stream));
+        else
+            CK(launch_rows_from_int(I->d, nullptr, din[b], I->ev_rows.as<uint8_t>(), c, I->stream));
+        g_launches += 1;
+        CK(cudaEventRecord(I->in_free[b], I->stream));
+        eval_rows(I, I->ev_rows.as<uint8_t>(), c, robj + first, rfit + first, rmk + first, rtd + first, true,
+                  errs + k);
+    }
+    std::vector<unsigned long long> codes((size_t)nsub);
+    CK(cudaMemcpyAsync(codes.data(), errs, sizeof(unsigned long long) * (size_t)nsub, cudaMemcpyDeviceToHost, I->stream));
+    CK(cudaMemcpyAsync(obj, robj, sizeof(double) * n, cudaMemcpyDeviceToHost, I->stream));
+    CK(cudaMemcpyAsync(fit, rfit, sizeof(double) * n, cudaMemcpyDeviceToHost, I->stream));
+    if (mk) CK(cudaMemcpyAsync(mk, rmk, sizeof(double) * n, cudaMemcpyDeviceToHost, I->stream));
+    if (td) CK(cudaMemcpyAsync(td, rtd, sizeof(double) * n, cudaMemcpyDeviceToHost, I->stream));
+    CK(cudaStreamSynchronize(I->stream));
+    for (unsigned long long code : codes)  // the first chromosome in batch order with a bad gene
+        if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
 }
 
 }  // namespace
