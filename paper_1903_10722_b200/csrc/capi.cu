@@ -193,6 +193,7 @@ struct ffsga_cuda_instance_t {
     cudaStream_t cstream = nullptr;
     cudaEvent_t pin_free[2] = {nullptr, nullptr}, in_ready[2] = {nullptr, nullptr}, in_free[2] = {nullptr, nullptr};
     DevBuf ev_in2, ev_res, ev_errs;
+    DevBuf sched;  // K7 schedule of ffsga_cuda_decode (machine, start, completion)
     // migration scratch
     DevBuf mg_keys0, mg_keys1, mg_idx0, mg_idx_a, mg_idx_b, mg_temp;
     // timing: event pairs recorded around launches, resolved lazily (no sync in the timed path)
@@ -714,10 +715,12 @@ int ffsga_cuda_decode(ffsga_cuda_instance inst, const int32_t* genes, int32_t* m
         ffsga_cuda_instance_t* I = inst;
         const size_t L = (size_t)I->J * I->S;
         ensure_eval_staging(I, 1);
-        DevBuf sm, ss, sc;
-        sm.alloc(L * sizeof(int32_t));
-        ss.alloc(L * sizeof(double));
-        sc.alloc(L * sizeof(double));
+        // the schedule lives in the instance (grown once): no allocation or device-wide
+        // synchronisation per call
+        I->sched.ensure(L * (sizeof(int32_t) + 2 * sizeof(double)) + 16);
+        int32_t* smach = reinterpret_cast<int32_t*>(I->sched.p);
+        double* sstart = reinterpret_cast<double*>(I->sched.as<char>() + ((L * sizeof(int32_t) + 15) & ~size_t(15)));
+        double* scomp = sstart + L;
         CK(cudaMemcpyAsync(I->ev_in.p, genes, L * sizeof(int32_t), cudaMemcpyHostToDevice, I->stream));
         CK(launch_rows_from_int(I->d, I->ev_in.as<int32_t>(), nullptr, I->ev_rows.as<uint8_t>(), 1, I->stream));
         I->ev_err.ensure(sizeof(unsigned long long));
@@ -731,22 +734,24 @@ int ffsga_cuda_decode(ffsga_cuda_instance inst, const int32_t* genes, int32_t* m
         W.mk = I->ev_mk.as<double>();
         W.td = I->ev_td.as<double>();
         W.err = I->ev_err.as<unsigned long long>();
-        W.smachine = sm.as<int>();
-        W.sstart = ss.as<double>();
-        W.scomp = sc.as<double>();
+        W.smachine = smach;
+        W.sstart = sstart;
+        W.scomp = scomp;
         CK(launch_eval(I->d, I->ec, W, 1, I->sm_count, true, I->stream));
         g_launches += 2;
         const unsigned long long code = read_error(I);
         if (code != kNoError) fail(FFSGA_ERR_CONTRACT, gene_error(code));
-        CK(cudaMemcpy(machine, sm.p, L * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(start, ss.p, L * sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(completion, sc.p, L * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(machine, smach, L * sizeof(int32_t), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(start, sstart, L * sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaMemcpyAsync(completion, scomp, L * sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+        CK(cudaStreamSynchronize(I->stream));
         if (report5) {
             double r[4];
-            CK(cudaMemcpy(&r[0], I->ev_mk.p, sizeof(double), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&r[1], I->ev_td.p, sizeof(double), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&r[2], I->ev_obj.p, sizeof(double), cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&r[3], I->ev_fit.p, sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(&r[0], I->ev_mk.p, sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+            CK(cudaMemcpyAsync(&r[1], I->ev_td.p, sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+            CK(cudaMemcpyAsync(&r[2], I->ev_obj.p, sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+            CK(cudaMemcpyAsync(&r[3], I->ev_fit.p, sizeof(double), cudaMemcpyDeviceToHost, I->stream));
+            CK(cudaStreamSynchronize(I->stream));
             report5[0] = r[0];
             report5[1] = r[1];
             report5[2] = r[2];
