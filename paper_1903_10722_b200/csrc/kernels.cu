@@ -1550,6 +1550,7 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
 template <int G>
 cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalItems& W, long long max_items,
                           int sm_count, bool schedule, cudaStream_t st) {
+    if (max_items <= 0 && !W.n_dev) return cudaSuccess;  // nothing to decode (an empty batch)
     long long blocks = (max_items + cfg.groups_per_cta - 1) / cfg.groups_per_cta;
     const long long cap = (long long)cfg.blocks_per_sm * sm_count;
     if (blocks > cap) blocks = cap;
