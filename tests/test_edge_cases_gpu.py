@@ -115,3 +115,58 @@ def test_extreme_weights_and_clamped_fitness(capi, orc, weight):
         obj, fit = inst.evaluate(pop)
         eo, ef, _, _ = oi.score_batch(pop, emax)
         assert np.array_equal(bits(obj), bits(eo)) and np.array_equal(bits(fit), bits(ef))
+
+
+def test_joint_step_mixed_island_sizes(capi, orc):
+    """One joint step over islands of different sizes and kinds (the work list interleaves their
+    cells and crossed members; graph replay for the small launches) equals each island stepped
+    alone by the C restatement."""
+    from conftest import synthetic
+    d = synthetic(orc, 30, 6, 2, 5)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    shapes = [(8, 4), (16, 16), (3, 2)]
+    cs = [capi.Cellular(inst, w, h, orc.derive_seed(6, i)) for i, (w, h) in enumerate(shapes)]
+    ocs = [oi.cellular(emax, w, h, orc.derive_seed(6, i)) for i, (w, h) in enumerate(shapes)]
+    sizes = [32, 64, 2]
+    ps = [capi.Pseudo(inst, n, orc.derive_seed(7, i)) for i, n in enumerate(sizes)]
+    ops = [oi.pseudo(emax, n, orc.derive_seed(7, i)) for i, n in enumerate(sizes)]
+    tc, tp = capi.step(cs, ps, 9)
+    for g in range(9):
+        for i, oc in enumerate(ocs):
+            oc.step()
+            assert tc[i, g] == oc.objective()[oc.best_index()]
+        for i, op in enumerate(ops):
+            op.step()
+            assert tp[i, g] == op.archive()[2]
+    for dc, oc in zip(cs, ocs):
+        assert np.array_equal(dc.genes(), oc.genes()) and np.array_equal(bits(dc.read()[0]), bits(oc.fitness()))
+    for dp, op in zip(ps, ops):
+        assert np.array_equal(dp.members(), op.members()) and dp.archive()[1] == op.archive()[1]
+
+
+def test_migrating_whole_islands(capi, orc):
+    """k = island population (migration.cpp:40-43 allows it): every member replaced, both ways,
+    locally and through device packets."""
+    d = orc.generate(8, 3, [2, 3, 2], weight=0.0, seed=5)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    dc, dp = capi.Cellular(inst, 4, 4, 3), capi.Pseudo(inst, 16, 4)
+    oc, op = oi.cellular(emax, 4, 4, 3), oi.pseudo(emax, 16, 4)
+    capi.step([dc], [dp], 2)
+    for _ in range(2):
+        oc.step()
+        op.step()
+    capi.migrate_cellular_to_pseudo(dc, dp, 16)
+    orc.lib.orc_migrate_cellular_to_pseudo(oc.ptr, op.ptr, 16)
+    assert np.array_equal(dp.members(), op.members()) and dp.archive()[1] == op.archive()[1]
+    capi.migrate_pseudo_to_cellular(dp, dc, 16)
+    orc.lib.orc_migrate_pseudo_to_cellular(op.ptr, oc.ptr, 16)
+    assert np.array_equal(dc.genes(), oc.genes()) and np.array_equal(bits(dc.read()[0]), bits(oc.fitness()))
+    dc2, dp2 = capi.Cellular(inst, 4, 4, 3), capi.Pseudo(inst, 16, 4)
+    capi.step([dc2], [dp2], 2)
+    dp2.import_packet(dc2.export_packet(16), 16)
+    dc2.import_packet(dp2.export_packet(16), 16)
+    assert np.array_equal(dc2.genes(), dc.genes()) and np.array_equal(dp2.members(), dp.members())
