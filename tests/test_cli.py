@@ -208,3 +208,27 @@ def test_result_and_trace_files_match_reference(tmp_path, ref):
         assert r["migrations"], "the fixture seeds fire migrations"
         assert _doc_without_timings(ours.read_text()) == _doc_without_timings(theirs.read_text())
         assert ours_tr.read_bytes() == theirs_tr.read_bytes()
+
+
+@pytest.mark.gpu
+def test_c2_run_files_match_reference(tmp_path, ref):
+    """C2: 100 x 10 x [2, 5], dual, population 4096 (grid 64 x 32 + 1024 pairs),
+    migration gap 500, 600 generations so the run crosses a rendezvous: the result JSON (outside
+    timings) and the trace CSV byte for byte against the compiled reference's run()
+    (proj/src/solver.cpp:58-164, proj/src/io.cpp)."""
+    from pyoracle import synthetic_machines
+    machines = synthetic_machines(100, 10, 2, 5)
+    inst = tmp_path / "c2.json"
+    assert run_cli("generate", "--jobs", 100, "--stages", 10, "--machines", ",".join(map(str, machines)),
+                   "--seed", 7, "--out", inst)[0] == 0
+    ours, ours_tr = tmp_path / "ours.json", tmp_path / "ours.csv"
+    code, _, err = run_cli("solve", "--instance", inst, "--population", 4096, "--generations", 600, "--gap", 500,
+                           "--seed", 1, "--out", ours, "--trace", ours_tr)
+    assert code == 0, err
+    d = ref.generate(100, 10, machines, weight=100.0, seed=7)
+    theirs, theirs_tr = tmp_path / "theirs.json", tmp_path / "theirs.csv"
+    r = ref.instance(d).run(population=4096, generations=600, gap=500, seed=1, workers=os.cpu_count() or 1,
+                            result_json=theirs, trace_csv=theirs_tr)
+    assert len(r["trace_combined"]) == 600
+    assert _doc_without_timings(ours.read_text()) == _doc_without_timings(theirs.read_text())
+    assert ours_tr.read_bytes() == theirs_tr.read_bytes()
