@@ -603,6 +603,16 @@ int ffsga_cuda_instance_create(int device, int num_jobs, int num_stages, const i
         }
         if (const char* v = std::getenv("FFSGA_EVAL_BSHIFT")) d.bshift = std::atoi(v);
         d.check_selftest = std::getenv("FFSGA_CHECK_SELFTEST") ? 1 : 0;
+        // Packed heads for K1's ready-only pass: a ready time's low bit_width(J) mantissa bits
+        // carry the job id, so one fp64 compare orders (ready, job) up to that truncation and the
+        // heads move one 64-bit word instead of a value and a job.  Needs sign-clear ready times
+        // (release -0.0 would order as a negative number) and a horizon far below the sentinel.
+        {
+            bool pk = J <= 65534 && horizon < 1e300;
+            for (int j = 0; j < J && pk; ++j) pk = !std::signbit(release[j]) && release[j] < 1e300;
+            d.pk_bits = pk ? bit_width_u((unsigned)J) : 0;
+            if (const char* v = std::getenv("FFSGA_EVAL_PK")) if (std::string(v) == "0") d.pk_bits = 0;
+        }
         if (const char* v = std::getenv("FFSGA_STEP_SPLIT")) I->step_split = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("FFSGA_STEP_MIX")) I->step_mix = std::max(0, std::atoi(v));
         mark("devinst");

@@ -114,6 +114,63 @@ __device__ __forceinline__ void heads_replace_min(double (&v)[NS], int (&j)[NS],
 }
 
 
+// ---- packed heads (K1's ready-only pass when DevInst::pk_bits > 0).  key = the ready time's
+// bits with the low pk_bits replaced by the job id.  For sign-clear finite ready times one fp64
+// compare of two keys orders them by (ready truncated above those bits, job): the exact
+// (ready, job) order except between ready times that agree above the job bits, which stage_pass
+// flags like a tie (exact re-decode).  The dropped bits of job j's ready time wait in a u16 array
+// (the link region, indexed by job) until j is popped.
+__device__ __forceinline__ double pk_pack(double v, int j, unsigned mask) {
+    return __hiloint2double(__double2hiint(v), (int)(((unsigned)__double2loint(v) & ~mask) | (unsigned)j));
+}
+__device__ __forceinline__ int pk_job(double k, unsigned mask) { return (int)((unsigned)__double2loint(k) & mask); }
+__device__ __forceinline__ unsigned pk_low(double v, unsigned mask) { return (unsigned)__double2loint(v) & mask; }
+__device__ __forceinline__ double pk_value(double k, unsigned low, unsigned mask) {
+    return __hiloint2double(__double2hiint(k), (int)(((unsigned)__double2loint(k) & ~mask) | low));
+}
+// above every real key (ready times < 1e300), job field END
+__device__ __forceinline__ double pk_sentinel(int end, unsigned mask) {
+    return __hiloint2double(0x7FEFFFFF, (int)((0xFFFFFFFFu & ~mask) | (unsigned)end));
+}
+// do two keys / ready times agree above the job bits?
+__device__ __forceinline__ bool pk_same_high(double a, double b, unsigned mask) {
+    return (__double2hiint(a) == __double2hiint(b)) &
+           ((((unsigned)__double2loint(a) ^ (unsigned)__double2loint(b)) & ~mask) == 0u);
+}
+
+template <int NS>
+__device__ __forceinline__ void heads_sort_pk(double (&v)[NS]) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+#pragma unroll
+        for (int k = NS - 1; k > i; --k) {
+            const double v0 = v[k - 1], v1 = v[k];
+            const bool sw = v1 < v0;
+            v[k - 1] = sw ? v1 : v0;
+            v[k] = sw ? v0 : v1;
+        }
+    }
+}
+
+// heads_replace_min on keys alone: two selects per 32-bit half per slot, no job ids
+template <int NS>
+__device__ __forceinline__ void heads_replace_min_pk(double (&v)[NS], double x) {
+    bool c[NS];
+#pragma unroll
+    for (int k = 0; k + 1 < NS; ++k) c[k] = v[k + 1] < x;
+    double nv[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const bool after = (k + 1 < NS) ? c[k] : false;
+        const bool here = (k == 0) ? true : c[k - 1];
+        const double keep = here ? x : v[k];
+        nv[k] = after ? v[(k + 1 < NS) ? k + 1 : k] : keep;
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[k] = nv[k];
+}
+
+
 __device__ __forceinline__ void stage_barrier(bool cta) {
     if (cta)
         __syncthreads();

@@ -24,6 +24,8 @@ struct DevInst {
     int algo;       // decoder: 0 = k-way merge of per-source lists, 1 = per-stage bucket sort
     int bshift;     // bucket decoder: J << bshift histogram buckets per stage
     int check_selftest;  // checked build: K1 reports a deliberate failure (proves the channel)
+    int pk_bits;    // K1 fast pass with packed heads: low pk_bits of a ready time's bits hold the
+                    // job id (0 = off; needs every ready time >= +0.0, see capi.cu)
     double weight, emax;
     const int* M;               // [S]
     const int* stage_off;       // [S+1]

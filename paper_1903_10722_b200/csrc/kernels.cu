@@ -45,7 +45,10 @@ namespace {
 // machine's fp64 recurrence start = max(ready, avail), completion = start + p (84-87) and
 // appends the job to its outgoing list (m -> gene of the next stage).  Branch-free body:
 // out-of-range next-stage genes land in lists nobody reads and are reported after the stage.
-template <int G, int NS, bool SCHED, bool LAST, bool EARLY, bool EXACT, int DEPTH>
+// PK: packed heads (decoder_common.cuh pk_*): node values are keys, the link region holds the
+// dropped low bits of each job's ready time (indexed by job), and the popped job comes out of
+// head 0's key; ready-only pass only (not EXACT, not SCHED).
+template <int G, int NS, bool SCHED, bool LAST, bool EARLY, bool EXACT, int DEPTH, bool PK>
 __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                            int m, bool work, double* __restrict__ lval,
                                            uint16_t* __restrict__ link, uint16_t* __restrict__ tail,
@@ -60,17 +63,32 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     asm volatile("" : "+l"(pcol));
     unsigned row_s = (unsigned)__cvta_generic_to_shared(row);
     asm volatile("" : "+r"(row_s));
+    static_assert(!PK || (!EXACT && !SCHED), "packed heads serve the ready-only pass");
+    const unsigned mask = PK ? (1u << I.pk_bits) - 1u : 0u;
     double hv[NS];
     int hj[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const bool live = work && m < Ms && k < Mprev;
         const int node = J + 1 + k * G + m;
-        hj[k] = live ? (int)link[node] : END;
-        hv[k] = live ? lval[node] : dinf();
-        FFSGA_CHECK(hj[k] <= END, 1, hj[k], s);
+        if (PK) {
+            hv[k] = live ? lval[node] : pk_sentinel(END, mask);
+            FFSGA_CHECK(pk_job(hv[k], mask) <= END, 1, pk_job(hv[k], mask), s);
+        } else {
+            hj[k] = live ? (int)link[node] : END;
+            hv[k] = live ? lval[node] : dinf();
+            FFSGA_CHECK(hj[k] <= END, 1, hj[k], s);
+        }
     }
-    heads_sort<NS>(hv, hj);
+    if (PK)
+        heads_sort_pk<NS>(hv);
+    else
+        heads_sort<NS>(hv, hj);
+    // the job at head 0
+    auto head = [&]() -> int {
+        if (PK) return pk_job(hv[0], mask);
+        return hj[0];
+    };
     uint16_t* mytail = tail + m * G;
     if (!last) {
 #pragma unroll
@@ -115,8 +133,13 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 const int d = min(q.g, G - 1);
                 const int t = mytail[d];
                 FFSGA_CHECK(t != END && t < J + 1 + G * G, 4, t, q.j);
-                link[t] = (uint16_t)q.j;
-                lval[t] = c;
+                if (PK) {
+                    lval[t] = pk_pack(c, q.j, mask);
+                    link[q.j] = (uint16_t)pk_low(c, mask);  // q.j's next ready time, low bits
+                } else {
+                    link[t] = (uint16_t)q.j;
+                    lval[t] = c;
+                }
                 mytail[d] = (uint16_t)q.j;
             } else {
                 lval[q.j] = c;  // final completion (the node was consumed by its pop)
@@ -131,7 +154,10 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         int ck_j = -1;
 #endif
         auto pop = [&](Pend& q, const Pend& prev, int bj) {
-            if (!EXACT) eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
+            if (PK)  // keys agreeing above the job bits: possibly out of (ready, job) order
+                eq |= pk_same_high(hv[0], prev.br, mask);
+            else if (!EXACT)
+                eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
 #ifdef FFSGA_CHECKED
             FFSGA_CHECK(bj >= 0 && bj < J, 2, bj, s);
             if (EXACT)
@@ -146,13 +172,17 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
 #endif
             int nh;
             double nr;
-            if (EARLY) {
+            if (PK) {  // the successor's key; bj's own ready time, low bits
+                nr = lval[bj];
+                nh = link[bj];
+            } else if (EARLY) {
                 nh = link[bj];
                 nr = lval[bj];
             }
-            FFSGA_CHECK(!EARLY || nh <= END, 3, nh, bj);
+            FFSGA_CHECK(PK || !EARLY || nh <= END, 3, nh, bj);
+            FFSGA_CHECK(!PK || pk_job(nr, mask) <= END, 3, pk_job(nr, mask), bj);
             if (q.j != END) retire(q);
-            q.br = hv[0];
+            q.br = PK ? pk_value(hv[0], (unsigned)nh, mask) : hv[0];
             q.p = __ldg(pcol + (unsigned)bj);  // unsigned index: one IMAD.WIDE.U32
             if (last) {
                 q.g = 0;
@@ -162,11 +192,14 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 q.g = (int)g;
             }
             q.j = bj;
-            if (!EARLY) {
+            if (!PK && !EARLY) {
                 nh = link[bj];
                 nr = lval[bj];
             }
-            heads_replace_min<NS, EXACT>(hv, hj, nr, nh);
+            if (PK)
+                heads_replace_min_pk<NS>(hv, nr);
+            else
+                heads_replace_min<NS, EXACT>(hv, hj, nr, nh);
         };
         if constexpr (DEPTH == 2 || DEPTH == 4) {
             bool a_older = true;  // which pending slot holds the older pop at loop exit
@@ -176,19 +209,19 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             // and the longer body schedules better (500x20 +2.4 %; at 100x10 the larger body
             // costs 11 %, so small instances keep the two-pop body)
             while (true) {
-                int bj = hj[0];
+                int bj = head();
                 if (bj == END) break;
                 pop(A, B, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     a_older = false;
                     break;
                 }
                 pop(B, A, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) break;
                 pop(A, B, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     a_older = false;
                     break;
@@ -197,10 +230,10 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             }
             } else {
             while (true) {
-                int bj = hj[0];
+                int bj = head();
                 if (bj == END) break;
                 pop(A, B, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     a_older = false;
                     break;
@@ -220,31 +253,31 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
             Pend C{qnan, 0.0, 0, END};
             int exit_at = 0;  // the slot the loop stopped before holds the oldest pending pop
             while (true) {  // unrolled six pops deep (see DEPTH 4)
-                int bj = hj[0];
+                int bj = head();
                 if (bj == END) break;
                 pop(A, C, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     exit_at = 1;
                     break;
                 }
                 pop(B, A, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     exit_at = 2;
                     break;
                 }
                 pop(C, B, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) break;
                 pop(A, C, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     exit_at = 1;
                     break;
                 }
                 pop(B, A, bj);
-                bj = hj[0];
+                bj = head();
                 if (bj == END) {
                     exit_at = 2;
                     break;
@@ -270,8 +303,12 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
 #pragma unroll
             for (int d = 0; d < G; ++d) {
                 const int t = mytail[d];
-                link[t] = (uint16_t)END;
-                lval[t] = dinf();
+                if (PK) {
+                    lval[t] = pk_sentinel(END, mask);
+                } else {
+                    link[t] = (uint16_t)END;
+                    lval[t] = dinf();
+                }
             }
         }
     }
@@ -292,7 +329,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
     stage_barrier(I.cta_sync);
 }
 
-template <int G, bool SCHED, bool EARLY, bool EXACT, int DEPTH>
+template <int G, bool SCHED, bool EARLY, bool EXACT, int DEPTH, bool PK>
 __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mprev, int Ms, int Mnext,
                                                int m, bool work, double* lval, uint16_t* link,
                                                uint16_t* tail, const uint8_t* row, const EvalItems& W,
@@ -301,10 +338,10 @@ __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mpre
     if constexpr (NS_ <= G) {                                                                       \
         if (Mprev <= NS_) {                                                                         \
             if (Mnext)                                                                              \
-                stage_pass<G, NS_, SCHED, false, EARLY, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                stage_pass<G, NS_, SCHED, false, EARLY, EXACT, DEPTH, PK>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
                                                                row, W, tie);                        \
             else                                                                                    \
-                stage_pass<G, NS_, SCHED, true, EARLY, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
+                stage_pass<G, NS_, SCHED, true, EARLY, EXACT, DEPTH, PK>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, \
                                                               row, W, tie);                         \
             return;                                                                                 \
         }                                                                                           \
@@ -325,24 +362,27 @@ __device__ __forceinline__ void dispatch_stage(const DevInst& I, int s, int Mpre
 // Out-of-range genes of stage s+1 (rare): walk lane m's outgoing lists (their nodes carry each
 // job's stage-s completion) and return the first offender in stage s+1 dispatch order, i.e.
 // the minimum (completion, job) among jobs whose next-stage gene is >= Mnext.
-template <int G>
+template <int G, bool PK>
 __device__ __forceinline__ void find_bad(const DevInst& I, int m, int Ms, int Mnext, const double* lval,
                                          const uint16_t* link, const uint8_t* row, BadTrack& bad) {
     const int J = I.J;
+    const unsigned mask = PK ? (1u << I.pk_bits) - 1u : 0u;
     if (m >= Ms) return;
     for (int d = 0; d < G; ++d) {
         int node = J + 1 + m * G + d;
         while (true) {
-            const int j = link[node];
+            const int j = PK ? pk_job(lval[node], mask) : (int)link[node];
             if (j == J) break;
-            if (row[j] >= Mnext) bad.consider(lval[node], j);
+            if (row[j] >= Mnext) bad.consider(PK ? pk_value(lval[node], link[j], mask) : lval[node], j);
             node = j;
         }
     }
 }
 
-template <int G, bool SCHED, int DEPTH>
-__global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
+// (512, 1): without the explicit minimum ptxas may cap the small-body variants at 64 registers
+// (with spills) to fit two 512-thread CTAs, which the shared-memory budget never allows anyway
+template <int G, bool SCHED, int DEPTH, bool PK>
+__global__ void __launch_bounds__(512, 1) k_eval(DevInst I, EvalItems W, int groups_per_cta, GroupLayout GL) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int gw = lane / G;
@@ -375,6 +415,8 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
         // reports equal consecutive ready times under the ready-only pop order.
         auto decode = [&](auto exact_tag, bool& work, bool& tie, unsigned long long& errc) {
             constexpr bool EXACT = decltype(exact_tag)::value;
+            constexpr bool PKD = PK && !EXACT;  // packed heads in the ready-only pass
+            const unsigned mask = PKD ? (1u << I.pk_bits) - 1u : 0u;
             if (work) prefetch_row<G>(I, genes, 0, m, row_a);
             tail[m] = (uint16_t)(J + 1 + m);  // virtual source 0 -> machine m of stage 0
             __pipeline_wait_prior(0);
@@ -403,8 +445,13 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
                 __syncwarp();
                 if (good) {
                     const int node = below ? pred_j : t;
-                    link[node] = (uint16_t)j;
-                    lval[node] = rel;
+                    if (PKD) {
+                        lval[node] = pk_pack(rel, j, mask);
+                        link[j] = (uint16_t)pk_low(rel, mask);
+                    } else {
+                        link[node] = (uint16_t)j;
+                        lval[node] = rel;
+                    }
                 }
                 if (good && !above) tail[d] = (uint16_t)j;
                 __syncwarp();
@@ -412,8 +459,12 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
             if (work) {
                 const int t = tail[m];
                 FFSGA_CHECK(t != END && t < J + 1 + G * G, 10, t, m);
-                link[t] = (uint16_t)END;
-                lval[t] = dinf();
+                if (PKD) {
+                    lval[t] = pk_sentinel(END, mask);
+                } else {
+                    link[t] = (uint16_t)END;
+                    lval[t] = dinf();
+                }
             }
             bad_k = group_min_int<G>(bad_k);
             if (work && bad_k != 0x7FFFFFFF) {
@@ -436,13 +487,13 @@ __global__ void __launch_bounds__(512) k_eval(DevInst I, EvalItems W, int groups
                 __syncwarp();
                 bool row_bad = false;
                 if (Mnext) row_bad = row_has_bad<G>(I, row, m, Mnext, work);
-                dispatch_stage<G, SCHED, true, EXACT, DEPTH>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row, W,
-                                                       tie);
+                dispatch_stage<G, SCHED, true, EXACT, DEPTH, PKD>(I, s, Mprev, Ms, Mnext, m, work, lval, link, tail, row,
+                                                             W, tie);
                 if (__any_sync(kFull, row_bad)) {
                     // first offending job in stage s+1 dispatch order: min (ready, job) among them
                     BadTrack bad;
                     bad.reset();
-                    if (row_bad && work) find_bad<G>(I, m, Ms, Mnext, lval, link, row, bad);
+                    if (row_bad && work) find_bad<G, PKD>(I, m, Ms, Mnext, lval, link, row, bad);
                     double bc = bad.c;
                     int bj = bad.j;
                     group_min_key<G>(bc, bj);
@@ -1518,7 +1569,10 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
     // Pop pipeline depth: three pops in flight for large instances (1000x20: +5 %), two
     // otherwise (500x20: the third slot costs 1.5 %; 100x10: -32 %, registers bind there)
     cfg->depth = 2;
-    const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false, 2>;
+    const void* k0 = I.algo == 1 ? (const void*)k_eval_bkt<G, false> : (const void*)k_eval<G, false, 2, false>;
+    if constexpr (G <= 8) {
+        if (I.algo != 1 && I.pk_bits) k0 = (const void*)k_eval<G, false, 2, true>;
+    }
     if constexpr (G == 8) {
         const char* dv = getenv("FFSGA_EVAL_DEPTH");  // experiments: 2, 3 or 4
         // measured thresholds (C5 shapes, M in [2, 8]): the 4-deep body wins from J = 300 on
@@ -1526,13 +1580,13 @@ int eval_config_g(const DevInst& I, int sm_count, int warps_cap, EvalConfig* cfg
         const int want = dv ? atoi(dv) : (I.J >= 1000 ? 3 : (I.J >= 300 ? 4 : 2));
         if (I.algo != 1 && want == 3) {
             cfg->depth = 3;
-            k0 = (const void*)k_eval<8, false, 3>;
+            k0 = I.pk_bits ? (const void*)k_eval<8, false, 3, true> : (const void*)k_eval<8, false, 3, false>;
         } else if (I.algo != 1 && want == 4) {
             cfg->depth = 4;
-            k0 = (const void*)k_eval<8, false, 4>;
+            k0 = I.pk_bits ? (const void*)k_eval<8, false, 4, true> : (const void*)k_eval<8, false, 4, false>;
         }
     }
-    const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true, 2>;
+    const void* k1 = I.algo == 1 ? (const void*)k_eval_bkt<G, true> : (const void*)k_eval<G, true, 2, false>;
     // the opt-in ceiling, not this config's size: configs of other instances (other J) and the
     // joint-step config share the kernel's attribute
     cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -1577,19 +1631,32 @@ cudaError_t launch_eval_g(const DevInst& I, const EvalConfig& cfg, const EvalIte
         else
             k_eval_bkt<G, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.bl);
     } else if (schedule) {
-        k_eval<G, true, 2><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+        k_eval<G, true, 2, false><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
     } else {
+        const dim3 grid((unsigned)blocks), block(32 * cfg.warps);
         if constexpr (G == 8) {
             if (cfg.depth == 3) {
-                k_eval<8, false, 3><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                if (I.pk_bits)
+                    k_eval<8, false, 3, true><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                else
+                    k_eval<8, false, 3, false><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
                 return cudaGetLastError();
             }
             if (cfg.depth == 4) {
-                k_eval<8, false, 4><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                if (I.pk_bits)
+                    k_eval<8, false, 4, true><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                else
+                    k_eval<8, false, 4, false><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
                 return cudaGetLastError();
             }
         }
-        k_eval<G, false, 2><<<(unsigned)blocks, 32 * cfg.warps, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+        if constexpr (G <= 8) {
+            if (I.pk_bits) {
+                k_eval<G, false, 2, true><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
+                return cudaGetLastError();
+            }
+        }
+        k_eval<G, false, 2, false><<<grid, block, cfg.smem, st>>>(I, W, cfg.groups_per_cta, cfg.gl);
     }
     return cudaGetLastError();
 }

@@ -170,3 +170,25 @@ def test_migrating_whole_islands(capi, orc):
     dp2.import_packet(dc2.export_packet(16), 16)
     dc2.import_packet(dp2.export_packet(16), 16)
     assert np.array_equal(dc2.genes(), dc.genes()) and np.array_equal(dp2.members(), dp.members())
+
+
+@pytest.mark.parametrize("pk", ["1", "0"])
+def test_packed_heads_near_ties(capi, orc, monkeypatch, pk):
+    """Ready times a few ulps apart agree above the job bits the packed heads keep (K1's
+    ready-only pass, DevInst::pk_bits): such pops are flagged and the chromosome is decoded again
+    in exact (ready, job) order.  Processing times n + k * 2^-48 make completions collide or miss
+    each other by ulps on every stage; with FFSGA_EVAL_PK=0 the unpacked pass runs instead."""
+    monkeypatch.setenv("FFSGA_EVAL_PK", pk)
+    rng = np.random.default_rng(31)
+    J, S, M = 48, 4, [3, 2, 4, 2]
+    proc = rng.integers(1, 5, size=(J, sum(M))) + rng.integers(0, 4, size=(J, sum(M))) * 2.0 ** -48
+    release = rng.integers(0, 3, J) + rng.integers(0, 8, J) * 2.0 ** -50
+    d = InstanceData(J, S, M, proc, release, release + 40.0, 1.0)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    pop = oi.random_population(6, 0, 400)
+    obj, fit, mk, td = inst.evaluate(pop, full=True)
+    eo, ef, em, et = oi.score_batch(pop, emax)
+    for a, e in ((obj, eo), (fit, ef), (mk, em), (td, et)):
+        assert np.array_equal(bits(a), bits(e))
