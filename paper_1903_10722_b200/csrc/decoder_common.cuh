@@ -132,10 +132,10 @@ __device__ __forceinline__ double pk_value(double k, unsigned low, unsigned mask
 __device__ __forceinline__ double pk_sentinel(int end, unsigned mask) {
     return __hiloint2double(0x7FEFFFFF, (int)((0xFFFFFFFFu & ~mask) | (unsigned)end));
 }
-// do two keys / ready times agree above the job bits?
-__device__ __forceinline__ bool pk_same_high(double a, double b, unsigned mask) {
-    return (__double2hiint(a) == __double2hiint(b)) &
-           ((((unsigned)__double2loint(a) ^ (unsigned)__double2loint(b)) & ~mask) == 0u);
+// zero iff two keys / ready times agree above the job bits (two LOP3s)
+__device__ __forceinline__ unsigned pk_high_diff(double a, double b, unsigned mask) {
+    return ((unsigned)__double2hiint(a) ^ (unsigned)__double2hiint(b)) |
+           (((unsigned)__double2loint(a) ^ (unsigned)__double2loint(b)) & ~mask);
 }
 
 template <int NS>

@@ -119,6 +119,9 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
         const double qnan = __longlong_as_double(0x7FF8000000000000LL);
         Pend A{qnan, 0.0, 0, END}, B{qnan, 0.0, 0, END};
         bool eq = false;  // two consecutive pops with equal ready times (ready-only order)
+        // PK: minimum over pops of the bits in which a pop's key differs from the previous pop's
+        // ready time above the job bits; 0 = the two agree there (possibly out of order)
+        unsigned tacc = 0xFFFFFFFFu;
         auto retire = [&](const Pend& q) {
             const double start = (q.br < avail) ? avail : q.br;  // std::max(ready, avail)
             const double c = __dadd_rn(start, q.p);
@@ -155,7 +158,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
 #endif
         auto pop = [&](Pend& q, const Pend& prev, int bj) {
             if (PK)  // keys agreeing above the job bits: possibly out of (ready, job) order
-                eq |= pk_same_high(hv[0], prev.br, mask);
+                tacc = min(tacc, pk_high_diff(hv[0], prev.br, mask));
             else if (!EXACT)
                 eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
 #ifdef FFSGA_CHECKED
@@ -241,7 +244,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 pop(B, A, bj);
             }
             }
-            tie |= eq;
+            tie |= eq | (tacc == 0u);
             if (a_older) {
                 if (A.j != END) retire(A);
                 if (B.j != END) retire(B);
@@ -284,7 +287,7 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 }
                 pop(C, B, bj);
             }
-            tie |= eq;
+            tie |= eq | (tacc == 0u);
             if (exit_at == 0) {
                 if (A.j != END) retire(A);
                 if (B.j != END) retire(B);
