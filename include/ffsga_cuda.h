@@ -71,7 +71,9 @@ int ffsga_cuda_instance_info(ffsga_cuda_instance inst, int* row_stride, int* gro
  * model.cpp:192-195) applied to n chromosomes.  genes: n * J*S job-major int32.  Outputs are
  * n doubles each; makespan / tardiness may be NULL.  An out-of-range gene makes the call fail
  * with FFSGA_ERR_CONTRACT and the reference message of the first offending chromosome
- * ("decode: machine index out of range at job J stage S", model.cpp:81-83). */
+ * ("decode: machine index out of range at job J stage S", model.cpp:81-83).
+ * A genes buffer in page-locked host memory (cudaHostAlloc / cudaHostRegister) is read in place
+ * by the copy engine; pageable buffers go through the library's pinned staging pair. */
 int ffsga_cuda_evaluate(ffsga_cuda_instance inst, const int32_t* genes, int64_t n, double* objective,
                         double* fitness, double* makespan, double* tardiness);
 /* Same with one byte per gene (the compact host layout of the e2e decoder benchmark). */

@@ -364,9 +364,26 @@ void staged_copy(void* dst, const void* src, size_t bytes) {
     for (auto& x : th) x.join();
 }
 
+// Is [p, p + bytes) in memory the copy engines can read in place (page-locked host memory, or
+// device / managed memory)?  Both ends are checked; pageable memory reports "unregistered".
+bool dma_readable(const void* p, size_t bytes) {
+    for (const void* q : {p, (const void*)((const char*)p + bytes - 1)}) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (a.type != cudaMemoryTypeHost && a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+            return false;
+    }
+    return true;
+}
+
 // Evaluator::score over a host batch, pipelined in sub-batches: the host copies sub-batch k+1
 // into pinned staging while the copy stream moves sub-batch k to the device and the instance
 // stream transposes and decodes the one before; results stay on the device until one copy back.
+// A batch already in page-locked (or device) memory skips the staging copy: the copy engine
+// reads it in place.
 template <typename T>
 void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* obj, double* fit, double* mk,
                    double* td) {
@@ -378,6 +395,7 @@ void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* 
     const long long sub = std::min<long long>(n, std::max<long long>(8192, (64ll << 20) / (L * (long long)sizeof(T))));
     const long long nsub = (n + sub - 1) / sub;
     const size_t in_bytes = (size_t)sub * L * sizeof(T);
+    const bool direct = dma_readable(genes, (size_t)n * L * sizeof(T));
     ensure_eval_staging(I, sub);
     I->ev_in2.ensure(in_bytes);
     I->ev_res.ensure(sizeof(double) * 4 * (size_t)n);
@@ -388,7 +406,7 @@ void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* 
             for (cudaEvent_t* e : {&I->pin_free[k], &I->in_ready[k], &I->in_free[k]})
                 CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    if (I->pin_bytes < in_bytes) {
+    if (!direct && I->pin_bytes < in_bytes) {
         for (int k = 0; k < 2; ++k) {
             if (I->pin[k]) CK(cudaFreeHost(I->pin[k]));
             I->pin[k] = nullptr;
@@ -408,10 +426,13 @@ void evaluate_host(ffsga_cuda_instance_t* I, const T* genes, int64_t n, double* 
         const int b = (int)(k & 1);
         const long long first = k * sub, c = std::min<long long>(sub, n - first);
         const size_t bytes = (size_t)c * L * sizeof(T);
-        if (k >= 2) CK(cudaEventSynchronize(I->pin_free[b]));  // sub-batch k-2 has left staging
-        staged_copy(I->pin[b], genes + first * L, bytes);
+        if (!direct) {
+            if (k >= 2) CK(cudaEventSynchronize(I->pin_free[b]));  // sub-batch k-2 has left staging
+            staged_copy(I->pin[b], genes + first * L, bytes);
+        }
         if (k >= 2) CK(cudaStreamWaitEvent(I->cstream, I->in_free[b], 0));  // ... and its device input
-        CK(cudaMemcpyAsync(din[b], I->pin[b], bytes, cudaMemcpyHostToDevice, I->cstream));
+        CK(cudaMemcpyAsync(din[b], direct ? (const void*)(genes + first * L) : (const void*)I->pin[b], bytes,
+                           cudaMemcpyDefault, I->cstream));
         CK(cudaEventRecord(I->pin_free[b], I->cstream));
         CK(cudaEventRecord(I->in_ready[b], I->cstream));
         CK(cudaStreamWaitEvent(I->stream, I->in_ready[b], 0));

@@ -192,3 +192,28 @@ def test_packed_heads_near_ties(capi, orc, monkeypatch, pk):
     eo, ef, em, et = oi.score_batch(pop, emax)
     for a, e in ((obj, eo), (fit, ef), (mk, em), (td, et)):
         assert np.array_equal(bits(a), bits(e))
+
+
+def test_host_batch_from_page_locked_memory(capi, orc):
+    """A batch already in page-locked host memory is read in place by the copy engine (no
+    staging copy): three pipelined sub-batches, equal to the pageable path and to the oracle."""
+    import torch
+    d = orc.generate(40, 4, [2, 3, 4, 2], seed=9)
+    oi = orc.instance(d)
+    emax = oi.estimate_emax()
+    inst = capi.Instance.from_data(d, emax)
+    n = 2 * 8192 + 77
+    pop = oi.random_population(12, 0, n)
+    for dtype, tdtype in ((np.int32, torch.int32), (np.uint8, torch.uint8)):
+        pinned = torch.empty(pop.shape, dtype=tdtype, pin_memory=True).numpy()
+        pinned[:] = pop.astype(dtype)
+        obj, fit = inst.evaluate(pinned)
+        obj2, fit2 = inst.evaluate(np.array(pinned, copy=True))
+        assert np.array_equal(bits(obj), bits(obj2)) and np.array_equal(bits(fit), bits(fit2))
+    eo, ef, _, _ = oi.score_batch(pop, emax)
+    assert np.array_equal(bits(obj), bits(eo)) and np.array_equal(bits(fit), bits(ef))
+    bad = torch.empty(pop.shape, dtype=torch.int32, pin_memory=True).numpy()
+    bad[:] = pop
+    bad[8192 + 5, 3] = 7
+    with pytest.raises(ValueError):
+        inst.evaluate(bad)
