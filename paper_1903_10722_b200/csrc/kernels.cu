@@ -1044,6 +1044,16 @@ __device__ __forceinline__ unsigned long long shfl_max_u64(unsigned long long v)
     return v;
 }
 
+// Parent rows stream through K3 once (20 KB per cell); loading them without an L1 allocation keeps
+// the L1 of an SM shared with a K1 CTA of the other chain for that CTA's processing-time slice.
+__device__ __forceinline__ uint4 ld_row_stream(const uint4* p) {
+    uint4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 // One cell, one warp: writes the child rows and returns the number of stream draws consumed.
 __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, int cell, unsigned long long cs,
                                          const double* __restrict__ fit, const uint8_t* __restrict__ selq,
@@ -1106,12 +1116,12 @@ __device__ unsigned long long breed_cell(const DevInst& I, const CellIsland& C, 
     }
     for (; s < I.S;) {
         const int j0 = vr * 16;
-        uint4 a = __ldg(reinterpret_cast<const uint4*>(g1 + (size_t)s * I.Jpad) + vr);
+        uint4 a = ld_row_stream(reinterpret_cast<const uint4*>(g1 + (size_t)s * I.Jpad) + vr);
         if (crossed) {
             const int jlo = lo - s <= 0 ? 0 : ceil_div_S(lo - s);
             const int jhi = hi - s <= 0 ? 0 : ceil_div_S(hi - s);
             if (jlo < j0 + 16 && jhi > j0 && jlo < jhi) {
-                const uint4 b = __ldg(reinterpret_cast<const uint4*>(g2 + (size_t)s * I.Jpad) + vr);
+                const uint4 b = ld_row_stream(reinterpret_cast<const uint4*>(g2 + (size_t)s * I.Jpad) + vr);
                 const int b0 = jlo - j0, b1 = jhi - j0;
                 unsigned m;
                 m = byte_mask(b0, b1, 0);
