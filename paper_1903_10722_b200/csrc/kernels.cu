@@ -163,11 +163,17 @@ __device__ __forceinline__ void stage_pass(const DevInst& I, int s, int Mprev, i
                 eq |= hv[0] == prev.br;  // the pops are sorted by ready time: ties adjoin
 #ifdef FFSGA_CHECKED
             FFSGA_CHECK(bj >= 0 && bj < J, 2, bj, s);
-            if (EXACT)
+            if (EXACT) {
                 FFSGA_CHECK(key_lt(ck_v, ck_j, hv[0], bj), 6, bj, s);
-            else
+                ck_v = hv[0];
+            } else if (PK) {  // packed: sorted above the job bits (below them a flagged tie)
+                const double hi_part = pk_value(hv[0], 0u, mask);
+                FFSGA_CHECK(!(hi_part < ck_v), 5, bj, s);
+                ck_v = hi_part;
+            } else {
                 FFSGA_CHECK(!(hv[0] < ck_v), 5, bj, s);
-            ck_v = hv[0];
+                ck_v = hv[0];
+            }
             ck_j = bj;
             ck_n += 1;
             ck_s1 += (unsigned long long)bj;
