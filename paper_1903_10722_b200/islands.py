@@ -279,6 +279,9 @@ class IslandModel:
         self.device_plane = bool(getattr(self.comm, "device_tensors", False)) and \
             hasattr(capi.Cellular, "export_packet")
         self.device = device
+        if self.comm.world == 1 and hasattr(capi.Cellular, "state_device"):
+            import torch  # torch's CUDA state, used by the rendezvous statistics, set up here
+            torch.zeros(1, dtype=torch.float64, device=torch.device("cuda", device))
 
     # -- pieces -------------------------------------------------------------------------
     def _cells(self):
@@ -320,19 +323,25 @@ class IslandModel:
         copied on its GPU into one tensor that NCCL all-gathers; the host then reads the n x 4
         values the (host-side, solver.cpp:142-163) policy needs."""
         n, comm = self.cfg.n_islands, self.comm
-        if self.device_plane:
+        # one process with the device backend: the same device copies and a single read-back
+        # (per-island host reads cost a synchronisation each: 64 islands ~ 5 ms per rendezvous)
+        local_dev = comm.world == 1 and hasattr(self.capi.Cellular, "state_device")
+        if self.device_plane or local_dev:
             import torch
             vec = torch.zeros((n, 4), dtype=torch.float64, device=torch.device("cuda", self.device))
             vec[:, 2] = -1.0
             for i, isl in self.local.items():
                 isl.state_device(vec[i])
-            allv = comm.allgather_tensor(vec).cpu().numpy()
+            allv = comm.allgather_tensor(vec).cpu().numpy() if self.device_plane else vec.cpu().numpy()[None]
         else:
             vec = np.zeros((n, 4))
             vec[:, 2] = -1.0
             for i, isl in self.local.items():
                 _, bf, bo = isl.best()
-                af, ao = (isl.archive()[1], isl.archive()[2]) if self.cfg.kind(i) == "pseudo" else (-1.0, 0.0)
+                if self.cfg.kind(i) == "pseudo":
+                    _, af, ao = isl.archive()
+                else:
+                    af, ao = -1.0, 0.0
                 vec[i] = (bf, bo, af, ao)
             allv = comm.allgather(vec.reshape(-1)).reshape(comm.world, n, 4)
         return np.stack([allv[owner(i, n, comm.world), i] for i in range(n)])
